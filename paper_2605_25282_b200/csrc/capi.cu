@@ -1,0 +1,632 @@
+// capi.cu — the C ABI of include/vlbm_b200.h: batch lifecycle, the host
+// side of the run_sample loop (device-resident scheduling, host polls one
+// int per chunk of steps), and the post-processing entry points.
+//
+// There is no CPU fallback: every numeric result below is produced by the
+// sm_100a kernels in march.cu / post.cu; a CUDA failure is reported as
+// VLBM_E_CUDA.
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+#include "march.cuh"
+
+using vlbm_dev::MarchParams;
+using vlbm_dev::SampleCtl;
+
+namespace vlbm_impl {
+
+static thread_local std::string g_last_error;
+
+int set_error(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+}  // namespace vlbm_impl
+
+using vlbm_impl::set_error;
+
+#define CU(call)                                                                   \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess)                                                         \
+      return set_error(VLBM_E_CUDA, std::string(#call ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+struct vlbm_batch {
+  vlbm_grid g{};
+  vlbm_params p{};
+  int S = 0;
+  int device = 0;
+  MarchParams P{};
+  cudaStream_t stream = nullptr;
+  int* h_active = nullptr;  // pinned
+  double* d_a0 = nullptr;
+  double* d_face_tx = nullptr;
+  double* d_face_ty = nullptr;
+  // stats
+  bool timing = false;
+  long long launches = 0;
+  double ms_theta = 0, ms_advance = 0, ms_sched = 0;
+  std::vector<cudaEvent_t> ev;  // pool of events, pairs per timed launch
+  std::vector<int> ev_kind;     // 0 sched, 1 theta, 2 advance
+  int ev_used = 0;
+};
+
+namespace {
+
+int check_device(int device) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    return set_error(VLBM_E_CUDA, std::string("no CUDA device available (the VLBM path has no "
+                                              "CPU fallback): ") +
+                                      cudaGetErrorString(e));
+  if (device < 0 || device >= n) return set_error(VLBM_E_INVALID, "device index out of range");
+  CU(cudaSetDevice(device));
+  return VLBM_OK;
+}
+
+void free_batch(vlbm_batch* b) {
+  if (!b) return;
+  cudaSetDevice(b->device);
+  cudaFree(b->P.buf0);
+  cudaFree(b->P.buf1);
+  cudaFree(b->P.theta);
+  cudaFree(const_cast<double*>(b->P.inlet));
+  cudaFree(b->P.ctl);
+  cudaFree(b->P.n_active);
+  cudaFree(b->d_a0);
+  cudaFree(b->d_face_tx);
+  cudaFree(b->d_face_ty);
+  if (b->h_active) cudaFreeHost(b->h_active);
+  for (cudaEvent_t e : b->ev) cudaEventDestroy(e);
+  if (b->stream) cudaStreamDestroy(b->stream);
+  delete b;
+}
+
+// Allocates the batch and its device arrays; fields/inlet uploaded by caller.
+int alloc_batch(const vlbm_grid* g, const vlbm_params* p, int S, int device, vlbm_batch** out) {
+  if (!g || !p || !out) return set_error(VLBM_E_INVALID, "null argument");
+  if (S < 1) return set_error(VLBM_E_INVALID, "n_samples must be >= 1");
+  if (int rc = vlbm_impl::validate_grid(*g)) return rc;
+  if (int rc = vlbm_impl::validate_params(*p)) return rc;
+  if (int rc = check_device(device)) return rc;
+  auto* b = new vlbm_batch;
+  b->g = *g;
+  b->p = *p;
+  b->S = S;
+  b->device = device;
+  MarchParams& P = b->P;
+  P.nx = g->nx;
+  P.ny = g->ny;
+  P.pitch = g->nx;
+  P.S = S;
+  P.plane = (long long)P.ny * P.pitch;
+  P.sample_stride = vlbm_dev::kPlanes * P.plane;
+  P.dx = vlbm_impl::grid_dx(*g);
+  P.gamma = p->gamma;
+  P.gm1 = p->gamma - 1.0;
+  P.alpha = p->alpha;
+  P.w = 0.25 * (1.0 - p->alpha);
+  P.safety = p->safety;
+  P.kappa = p->rlmp_relaxation;
+  P.rho_ref = p->rho_ref;
+  P.p_ref = p->p_ref;
+  P.rho_floor_coef = p->positivity_floor * p->rho_ref;  // rlmp_bounds, solver.hpp:413-414
+  P.p_floor_coef = p->positivity_floor * p->p_ref;
+  for (int k = 0; k < 4; ++k) P.bc[k] = p->bc[k];
+  P.limiter = p->limiter;
+  P.conservative = p->conservative_bound;
+  const size_t state_bytes = sizeof(double) * (size_t)S * P.sample_stride;
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  const size_t need = 2 * state_bytes + sizeof(double) * (size_t)S * P.plane +
+                      sizeof(double) * (size_t)S * P.ny * 4 + sizeof(SampleCtl) * S;
+  if (need + (size_t)(256ull << 20) > free_b) {
+    delete b;
+    return set_error(VLBM_E_NOMEM, "batch needs " + std::to_string(need >> 20) + " MiB, " +
+                                       std::to_string(free_b >> 20) + " MiB free");
+  }
+  int rc = VLBM_OK;
+  auto chk = [&](cudaError_t e, const char* what) {
+    if (e != cudaSuccess && rc == VLBM_OK)
+      rc = set_error(VLBM_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  };
+  chk(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking), "stream");
+  chk(cudaMalloc(&P.buf0, state_bytes), "malloc state0");
+  chk(cudaMalloc(&P.buf1, state_bytes), "malloc state1");
+  chk(cudaMalloc(&P.theta, sizeof(double) * (size_t)S * P.plane), "malloc theta");
+  double* inlet = nullptr;
+  chk(cudaMalloc(&inlet, sizeof(double) * (size_t)S * P.ny * 4), "malloc inlet");
+  P.inlet = inlet;
+  chk(cudaMalloc(&P.ctl, sizeof(SampleCtl) * S), "malloc ctl");
+  chk(cudaMalloc(&P.n_active, sizeof(int)), "malloc n_active");
+  chk(cudaMalloc(&b->d_a0, sizeof(double) * S), "malloc a0");
+  chk(cudaMallocHost(&b->h_active, sizeof(int)), "malloc host");
+  if (rc == VLBM_OK) {
+    chk(cudaMemsetAsync(P.buf0, 0, state_bytes, b->stream), "memset");
+    chk(cudaMemsetAsync(P.buf1, 0, state_bytes, b->stream), "memset");
+    chk(cudaMemsetAsync(P.theta, 0, sizeof(double) * (size_t)S * P.plane, b->stream), "memset");
+    chk(cudaMemsetAsync(inlet, 0, sizeof(double) * (size_t)S * P.ny * 4, b->stream), "memset");
+    std::vector<SampleCtl> ctl(S);
+    std::memset(ctl.data(), 0, sizeof(SampleCtl) * S);
+    for (auto& c : ctl) c.status = vlbm_dev::ST_RUNNING;
+    chk(cudaMemcpyAsync(P.ctl, ctl.data(), sizeof(SampleCtl) * S, cudaMemcpyHostToDevice,
+                        b->stream),
+        "upload ctl");
+    chk(cudaStreamSynchronize(b->stream), "sync");
+  }
+  if (rc != VLBM_OK) {
+    free_batch(b);
+    return rc;
+  }
+  *out = b;
+  return VLBM_OK;
+}
+
+int upload_sample(vlbm_batch* b, int s, const double* field, const double* inlet_rows) {
+  const MarchParams& P = b->P;
+  const size_t n = (size_t)P.nx * P.ny;
+  double* dst = P.buf0 + (size_t)s * P.sample_stride;
+  for (int k = 0; k < 4; ++k)
+    CU(cudaMemcpy2DAsync(dst + k * P.plane, sizeof(double) * P.pitch, field + k * n,
+                         sizeof(double) * P.nx, sizeof(double) * P.nx, P.ny,
+                         cudaMemcpyHostToDevice, b->stream));
+  if (inlet_rows)
+    CU(cudaMemcpyAsync(const_cast<double*>(P.inlet) + (size_t)s * P.ny * 4, inlet_rows,
+                       sizeof(double) * P.ny * 4, cudaMemcpyHostToDevice, b->stream));
+  return VLBM_OK;
+}
+
+// Constructor tail: kinetic speed of the initial field, a0, pops = M(u, a0).
+int finish_create(vlbm_batch* b) {
+  CU(vlbm_impl::launch_signal(b->P, b->stream));
+  CU(vlbm_impl::launch_init(b->P, b->d_a0, b->stream));
+  b->launches += 3;
+  CU(cudaStreamSynchronize(b->stream));
+  return VLBM_OK;
+}
+
+void record(vlbm_batch* b, int kind) {
+  if (!b->timing) return;
+  while ((int)b->ev.size() < 2 * (b->ev_used + 1)) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    b->ev.push_back(e);
+  }
+  if ((int)b->ev_kind.size() < b->ev_used + 1) b->ev_kind.resize(b->ev_used + 1);
+  b->ev_kind[b->ev_used] = kind;
+  cudaEventRecord(b->ev[2 * b->ev_used], b->stream);
+}
+void record_end(vlbm_batch* b) {
+  if (!b->timing) return;
+  cudaEventRecord(b->ev[2 * b->ev_used + 1], b->stream);
+  ++b->ev_used;
+}
+void harvest(vlbm_batch* b) {
+  for (int q = 0; q < b->ev_used; ++q) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, b->ev[2 * q], b->ev[2 * q + 1]);
+    if (b->ev_kind[q] == 0)
+      b->ms_sched += ms;
+    else if (b->ev_kind[q] == 1)
+      b->ms_theta += ms;
+    else
+      b->ms_advance += ms;
+  }
+  b->ev_used = 0;
+}
+
+// The run_sample while-loop for every sample (solver.hpp:645-658), device
+// scheduled: chunks of `chunk` iterations [sched, theta, advance] are issued,
+// then the host reads the number of samples the last k_sched scheduled; 0
+// means every sample has reached the target (or diverged / used its budget)
+// and every step taken is finalised.
+int march_loop(vlbm_batch* b, double target, double fixed_dt, int mode, int chunk) {
+  const MarchParams& P = b->P;
+  const bool rlmp = b->p.limiter == VLBM_LIMITER_RLMP && mode == 0;
+  const int adv_mode = mode == 2 ? 2 : (rlmp ? 0 : 1);
+  const double const_theta = b->p.limiter == VLBM_LIMITER_SECOND_ORDER ? 1.0 : 0.0;
+  for (;;) {
+    for (int it = 0; it < chunk; ++it) {
+      record(b, 0);
+      CU(vlbm_impl::launch_sched(P, target, fixed_dt, b->stream));
+      record_end(b);
+      if (rlmp) {
+        record(b, 1);
+        CU(vlbm_impl::launch_theta(P, b->stream));
+        record_end(b);
+      }
+      record(b, 2);
+      CU(vlbm_impl::launch_advance(P, adv_mode, const_theta, b->stream));
+      record_end(b);
+      b->launches += rlmp ? 3 : 2;
+    }
+    CU(cudaMemcpyAsync(b->h_active, P.n_active, sizeof(int), cudaMemcpyDeviceToHost, b->stream));
+    CU(cudaStreamSynchronize(b->stream));
+    if (b->timing) harvest(b);
+    if (*b->h_active == 0) return VLBM_OK;
+    if (mode == 2) chunk = 1;
+  }
+}
+
+int read_ctl(vlbm_batch* b, std::vector<SampleCtl>& ctl) {
+  ctl.resize(b->S);
+  CU(cudaMemcpyAsync(ctl.data(), b->P.ctl, sizeof(SampleCtl) * b->S, cudaMemcpyDeviceToHost,
+                     b->stream));
+  CU(cudaStreamSynchronize(b->stream));
+  return VLBM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int vlbm_abi_version(void) { return VLBM_ABI_VERSION; }
+const char* vlbm_last_error(void) { return vlbm_impl::g_last_error.c_str(); }
+
+int vlbm_batch_create(const vlbm_grid* g, const vlbm_params* p, const vlbm_perturbation* pp,
+                      uint64_t base_seed, int64_t m0, int n_samples, double strip_width,
+                      int device, vlbm_batch** out) {
+  if (!pp) return set_error(VLBM_E_INVALID, "null perturbation");
+  if (int rc = vlbm_impl::validate_perturbation(*pp)) return rc;
+  if (strip_width < 0.0) return set_error(VLBM_E_INVALID, "config: inlet_strip_width must be >= 0");
+  // run_sample's construction (solver.hpp:633-640): jet boundaries and
+  // set_reference(rho_amb, p_amb).
+  vlbm_params q = *p;
+  q.bc[0] = VLBM_BC_INLET;
+  q.bc[1] = VLBM_BC_OUTFLOW;
+  q.bc[2] = VLBM_BC_WALL;
+  q.bc[3] = VLBM_BC_WALL;
+  q.rho_ref = pp->rho_amb;
+  q.p_ref = pp->p_amb;
+  vlbm_batch* b = nullptr;
+  if (int rc = alloc_batch(g, &q, n_samples, device, &b)) return rc;
+  const int K = pp->modes;
+  std::vector<double> yc(K), zc(K), rows(4 * (size_t)g->ny);
+  double* field = nullptr;
+  const size_t n = (size_t)g->nx * g->ny;
+  if (cudaMallocHost(&field, sizeof(double) * 4 * n) != cudaSuccess) {
+    free_batch(b);
+    return set_error(VLBM_E_NOMEM, "pinned staging buffer");
+  }
+  int rc = VLBM_OK;
+  for (int s = 0; s < n_samples && rc == VLBM_OK; ++s) {
+    vlbm_draw_coefficients(base_seed, (uint64_t)(m0 + s), K, yc.data(), zc.data());
+    for (int j = 0; j < g->ny; ++j)
+      vlbm_impl::inlet_state(vlbm_impl::y_center(*g, j), K, yc.data(), zc.data(), *pp, q.gamma,
+                             rows.data() + 4 * j);
+    vlbm_impl::initial_field(*g, K, yc.data(), zc.data(), *pp, q.gamma, strip_width, field);
+    rc = upload_sample(b, s, field, rows.data());
+    if (rc == VLBM_OK && cudaStreamSynchronize(b->stream) != cudaSuccess)
+      rc = set_error(VLBM_E_CUDA, "upload");
+  }
+  cudaFreeHost(field);
+  if (rc == VLBM_OK) rc = finish_create(b);
+  if (rc != VLBM_OK) {
+    free_batch(b);
+    return rc;
+  }
+  *out = b;
+  return VLBM_OK;
+}
+
+int vlbm_batch_create_fields(const vlbm_grid* g, const vlbm_params* p, int n_samples,
+                             const double* init_fields, const double* inlet_rows,
+                             const uint64_t* seeds, int device, vlbm_batch** out) {
+  (void)seeds;
+  if (!init_fields) return set_error(VLBM_E_INVALID, "Simulation: initial field size mismatch");
+  if (p && p->bc[0] == VLBM_BC_INLET && !inlet_rows)
+    return set_error(VLBM_E_INVALID, "Simulation: inlet boundary requires a profile");
+  vlbm_batch* b = nullptr;
+  if (int rc = alloc_batch(g, p, n_samples, device, &b)) return rc;
+  const size_t n = (size_t)g->nx * g->ny;
+  int rc = VLBM_OK;
+  for (int s = 0; s < n_samples && rc == VLBM_OK; ++s)
+    rc = upload_sample(b, s, init_fields + 4 * n * s,
+                       inlet_rows ? inlet_rows + (size_t)4 * g->ny * s : nullptr);
+  if (rc == VLBM_OK) rc = finish_create(b);
+  if (rc != VLBM_OK) {
+    free_batch(b);
+    return rc;
+  }
+  *out = b;
+  return VLBM_OK;
+}
+
+void vlbm_batch_destroy(vlbm_batch* b) { free_batch(b); }
+int vlbm_batch_size(const vlbm_batch* b) { return b ? b->S : 0; }
+
+int vlbm_batch_run_to(vlbm_batch* b, double target) {
+  if (!b) return set_error(VLBM_E_INVALID, "null batch");
+  CU(cudaSetDevice(b->device));
+  CU(vlbm_impl::launch_set_budget(b->P, LLONG_MAX, b->stream));
+  ++b->launches;
+  return march_loop(b, target, 0.0, 0, 16);
+}
+
+int vlbm_batch_step(vlbm_batch* b, int n, double fixed_dt) {
+  if (!b) return set_error(VLBM_E_INVALID, "null batch");
+  if (n <= 0) return VLBM_OK;
+  CU(cudaSetDevice(b->device));
+  CU(vlbm_impl::launch_set_budget(b->P, n, b->stream));
+  ++b->launches;
+  const double inf = std::numeric_limits<double>::infinity();
+  return march_loop(b, inf, fixed_dt > 0.0 ? fixed_dt : 0.0, 0, n < 16 ? n + 1 : 16);
+}
+
+int vlbm_batch_step_with_blending(vlbm_batch* b, double dt, const double* theta_x,
+                                  const double* theta_y) {
+  if (!b || !theta_x || !theta_y) return set_error(VLBM_E_INVALID, "null argument");
+  CU(cudaSetDevice(b->device));
+  const size_t ntx = (size_t)b->S * b->g.ny * (b->g.nx + 1);
+  const size_t nty = (size_t)b->S * (b->g.ny + 1) * b->g.nx;
+  if (!b->d_face_tx) {
+    CU(cudaMalloc(&b->d_face_tx, sizeof(double) * ntx));
+    CU(cudaMalloc(&b->d_face_ty, sizeof(double) * nty));
+  }
+  CU(cudaMemcpyAsync(b->d_face_tx, theta_x, sizeof(double) * ntx, cudaMemcpyHostToDevice,
+                     b->stream));
+  CU(cudaMemcpyAsync(b->d_face_ty, theta_y, sizeof(double) * nty, cudaMemcpyHostToDevice,
+                     b->stream));
+  b->P.face_tx = b->d_face_tx;
+  b->P.face_ty = b->d_face_ty;
+  CU(vlbm_impl::launch_set_budget(b->P, 1, b->stream));
+  ++b->launches;
+  const double inf = std::numeric_limits<double>::infinity();
+  return march_loop(b, inf, dt > 0.0 ? dt : 0.0, 2, 2);
+}
+
+int vlbm_batch_get(vlbm_batch* b, int s, double* u, double* pops, double* time, int64_t* steps,
+                   int* status) {
+  if (!b) return set_error(VLBM_E_INVALID, "null batch");
+  if (s < 0 || s >= b->S) return set_error(VLBM_E_INVALID, "sample index out of range");
+  CU(cudaSetDevice(b->device));
+  std::vector<SampleCtl> ctl;
+  if (int rc = read_ctl(b, ctl)) return rc;
+  const MarchParams& P = b->P;
+  const double* src = (ctl[s].parity ? P.buf1 : P.buf0) + (size_t)s * P.sample_stride;
+  const size_t n = (size_t)P.nx * P.ny;
+  if (u)
+    for (int k = 0; k < 4; ++k)
+      CU(cudaMemcpy2DAsync(u + k * n, sizeof(double) * P.nx, src + k * P.plane,
+                           sizeof(double) * P.pitch, sizeof(double) * P.nx, P.ny,
+                           cudaMemcpyDeviceToHost, b->stream));
+  if (pops)
+    for (int k = 0; k < 16; ++k)
+      CU(cudaMemcpy2DAsync(pops + k * n, sizeof(double) * P.nx, src + (4 + k) * P.plane,
+                           sizeof(double) * P.pitch, sizeof(double) * P.nx, P.ny,
+                           cudaMemcpyDeviceToHost, b->stream));
+  CU(cudaStreamSynchronize(b->stream));
+  if (time) *time = ctl[s].t;
+  if (steps) *steps = ctl[s].steps;
+  if (status) *status = ctl[s].status;
+  return VLBM_OK;
+}
+
+int vlbm_batch_get_fields(vlbm_batch* b, double* u_all) {
+  if (!b || !u_all) return set_error(VLBM_E_INVALID, "null argument");
+  CU(cudaSetDevice(b->device));
+  std::vector<SampleCtl> ctl;
+  if (int rc = read_ctl(b, ctl)) return rc;
+  const MarchParams& P = b->P;
+  const size_t n = (size_t)P.nx * P.ny;
+  for (int s = 0; s < b->S; ++s) {
+    const double* src = (ctl[s].parity ? P.buf1 : P.buf0) + (size_t)s * P.sample_stride;
+    for (int k = 0; k < 4; ++k)
+      CU(cudaMemcpy2DAsync(u_all + (4 * (size_t)s + k) * n, sizeof(double) * P.nx,
+                           src + k * P.plane, sizeof(double) * P.pitch, sizeof(double) * P.nx,
+                           P.ny, cudaMemcpyDeviceToHost, b->stream));
+  }
+  CU(cudaStreamSynchronize(b->stream));
+  return VLBM_OK;
+}
+
+int vlbm_batch_get_scalars(vlbm_batch* b, double* time, int64_t* steps, int* status) {
+  if (!b) return set_error(VLBM_E_INVALID, "null batch");
+  CU(cudaSetDevice(b->device));
+  std::vector<SampleCtl> ctl;
+  if (int rc = read_ctl(b, ctl)) return rc;
+  for (int s = 0; s < b->S; ++s) {
+    if (time) time[s] = ctl[s].t;
+    if (steps) steps[s] = ctl[s].steps;
+    if (status) status[s] = ctl[s].status;
+  }
+  return VLBM_OK;
+}
+
+int vlbm_batch_get_theta(vlbm_batch* b, int s, double* theta) {
+  if (!b || !theta) return set_error(VLBM_E_INVALID, "null argument");
+  if (s < 0 || s >= b->S) return set_error(VLBM_E_INVALID, "sample index out of range");
+  CU(cudaSetDevice(b->device));
+  const MarchParams& P = b->P;
+  CU(cudaMemcpy2DAsync(theta, sizeof(double) * P.nx, P.theta + (size_t)s * P.plane,
+                       sizeof(double) * P.pitch, sizeof(double) * P.nx, P.ny,
+                       cudaMemcpyDeviceToHost, b->stream));
+  CU(cudaStreamSynchronize(b->stream));
+  return VLBM_OK;
+}
+
+int vlbm_batch_device_u(vlbm_batch* b, int s, double** d_u) {
+  if (!b || !d_u) return set_error(VLBM_E_INVALID, "null argument");
+  if (s < 0 || s >= b->S) return set_error(VLBM_E_INVALID, "sample index out of range");
+  std::vector<SampleCtl> ctl;
+  if (int rc = read_ctl(b, ctl)) return rc;
+  *d_u = (ctl[s].parity ? b->P.buf1 : b->P.buf0) + (size_t)s * b->P.sample_stride;
+  return VLBM_OK;
+}
+
+void* vlbm_batch_stream(vlbm_batch* b) { return b ? (void*)b->stream : nullptr; }
+
+int vlbm_batch_set_timing(vlbm_batch* b, int enable) {
+  if (!b) return set_error(VLBM_E_INVALID, "null batch");
+  b->timing = enable != 0;
+  b->ms_theta = b->ms_advance = b->ms_sched = 0;
+  return VLBM_OK;
+}
+
+int vlbm_batch_stats(vlbm_batch* b, int64_t* launches, double* ms_theta, double* ms_advance,
+                     double* ms_sched, int64_t* cell_updates) {
+  if (!b) return set_error(VLBM_E_INVALID, "null batch");
+  if (launches) *launches = b->launches;
+  if (ms_theta) *ms_theta = b->ms_theta;
+  if (ms_advance) *ms_advance = b->ms_advance;
+  if (ms_sched) *ms_sched = b->ms_sched;
+  if (cell_updates) {
+    std::vector<SampleCtl> ctl;
+    if (int rc = read_ctl(b, ctl)) return rc;
+    long long tot = 0;
+    for (auto& c : ctl) tot += c.steps;
+    *cell_updates = tot * (long long)b->g.nx * b->g.ny;
+  }
+  return VLBM_OK;
+}
+
+// ---- post-processing, host buffers -------------------------------------------
+
+namespace {
+struct DevBuf {
+  double* p = nullptr;
+  ~DevBuf() { cudaFree(p); }
+  cudaError_t alloc(size_t n) { return cudaMalloc(&p, sizeof(double) * (n ? n : 1)); }
+};
+int upload(DevBuf& d, const double* h, size_t n) {
+  CU(d.alloc(n));
+  CU(cudaMemcpy(d.p, h, sizeof(double) * n, cudaMemcpyHostToDevice));
+  return VLBM_OK;
+}
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return check_device(dev);
+}
+}  // namespace
+
+int vlbm_restrict_field(int nx, int ny, const double* fine, double* coarse) {
+  if (nx % 2 != 0 || ny % 2 != 0)
+    return set_error(VLBM_E_INVALID, "restrict_field: fine dimensions must be even");
+  if (int rc = current_device()) return rc;
+  const size_t nf = (size_t)4 * nx * ny, nc = nf / 4;
+  DevBuf df, dc;
+  if (int rc = upload(df, fine, nf)) return rc;
+  CU(dc.alloc(nc));
+  CU(vlbm_impl::launch_restrict(1, nx / 2, ny / 2, df.p, dc.p, 0));
+  CU(cudaMemcpy(coarse, dc.p, sizeof(double) * nc, cudaMemcpyDeviceToHost));
+  return VLBM_OK;
+}
+
+// Host tail of strong_error (metrics.hpp:81-89) over the device partials.
+static int strong_finish(int M, const std::vector<double>& part, double* result, double* pc) {
+  double acc = 0.0;
+  double comp_acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int m = 0; m < M; ++m) {
+    const double* o = part.data() + 10 * (size_t)m;
+    if (o[1] == 0.0) return set_error(VLBM_E_DOMAIN, "strong_error: zero reference norm");
+    acc += o[0] / o[1];
+    for (int k = 0; k < 4; ++k) comp_acc[k] += o[6 + k] > 0.0 ? o[2 + k] / o[6 + k] : 0.0;
+  }
+  if (pc)
+    for (int k = 0; k < 4; ++k) pc[k] = comp_acc[k] / static_cast<double>(M);
+  *result = acc / static_cast<double>(M);
+  return VLBM_OK;
+}
+
+int vlbm_strong_error(int M, int64_t n, const double* a, const double* b, double* result,
+                      double* pc) {
+  if (M < 1 || !a || !b || !result)
+    return set_error(VLBM_E_INVALID, "strong_error: sample counts differ or are empty");
+  if (int rc = current_device()) return rc;
+  DevBuf da, db, dp;
+  if (int rc = upload(da, a, (size_t)4 * n * M)) return rc;
+  if (int rc = upload(db, b, (size_t)4 * n * M)) return rc;
+  CU(dp.alloc(10 * (size_t)M));
+  CU(vlbm_impl::launch_strong_partials(M, n, da.p, db.p, dp.p, 0));
+  std::vector<double> part(10 * (size_t)M);
+  CU(cudaMemcpy(part.data(), dp.p, sizeof(double) * part.size(), cudaMemcpyDeviceToHost));
+  return strong_finish(M, part, result, pc);
+}
+
+int vlbm_wasserstein1(int M, int64_t n, const double* a, const double* b, int var,
+                      double* result) {
+  if (M < 1 || !a || !b || !result)
+    return set_error(VLBM_E_INVALID, "wasserstein1: sample counts differ or are empty");
+  if (var < 0 || var > 3) return set_error(VLBM_E_INVALID, "variable must be 0..3");
+  if (M > 1024) return set_error(VLBM_E_INVALID, "wasserstein1: M > 1024 not supported");
+  if (int rc = current_device()) return rc;
+  DevBuf da, db, dt, dr;
+  if (int rc = upload(da, a, (size_t)4 * n * M)) return rc;
+  if (int rc = upload(db, b, (size_t)4 * n * M)) return rc;
+  CU(dt.alloc(n));
+  CU(dr.alloc(1));
+  CU(vlbm_impl::launch_w1_planes(M, n, da.p + var * n, 4 * n, db.p + var * n, 4 * n, dt.p, 0));
+  CU(vlbm_impl::launch_ordered_mean(n, dt.p, dr.p, 0));
+  CU(cudaMemcpy(result, dr.p, sizeof(double), cudaMemcpyDeviceToHost));
+  return VLBM_OK;
+}
+
+int vlbm_ensemble_moments(int M, int64_t n, const double* x, double* mean, double* sd) {
+  if (M < 1 || !x) return set_error(VLBM_E_INVALID, "ensemble_moments: no samples");
+  if (M < 2)
+    return set_error(VLBM_E_INVALID, "ensemble_moments: std requires at least 2 samples");
+  if (int rc = current_device()) return rc;
+  DevBuf dx, dm, ds;
+  if (int rc = upload(dx, x, (size_t)4 * n * M)) return rc;
+  CU(dm.alloc(4 * n));
+  CU(ds.alloc(4 * n));
+  CU(vlbm_impl::launch_moments(M, 4 * n, dx.p, 4 * n, dm.p, ds.p, 0));
+  CU(cudaMemcpy(mean, dm.p, sizeof(double) * 4 * n, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(sd, ds.p, sizeof(double) * 4 * n, cudaMemcpyDeviceToHost));
+  return VLBM_OK;
+}
+
+// ---- post-processing, device buffers (stream-ordered) ------------------------
+
+int vlbm_d_strong_partials(int M, int nxc, int nyc, const double* d_coarse, const double* d_fine,
+                           double* d_partials, void* stream) {
+  CU(vlbm_impl::launch_strong_partials_fused(M, nxc, nyc, d_coarse, d_fine, d_partials,
+                                             (cudaStream_t)stream));
+  return VLBM_OK;
+}
+
+int vlbm_d_restrict_var(int M, int nxc, int nyc, const double* d_fine, int var, double* d_out,
+                        void* stream) {
+  CU(vlbm_impl::launch_restrict_var(M, nxc, nyc, d_fine, var, d_out, (cudaStream_t)stream));
+  return VLBM_OK;
+}
+
+int vlbm_d_w1_cells(int M, int64_t n, const double* d_a, const double* d_b, double* d_terms,
+                    void* stream) {
+  if (M < 1 || M > 1024) return set_error(VLBM_E_INVALID, "wasserstein1: 1 <= M <= 1024");
+  CU(vlbm_impl::launch_w1_cells(M, n, d_a, d_b, d_terms, (cudaStream_t)stream));
+  return VLBM_OK;
+}
+
+int vlbm_d_w1_cells_planes(int M, int64_t n, const double* d_a, const double* d_b,
+                           double* d_terms, void* stream) {
+  if (M < 1 || M > 1024) return set_error(VLBM_E_INVALID, "wasserstein1: 1 <= M <= 1024");
+  CU(vlbm_impl::launch_w1_planes(M, n, d_a, n, d_b, n, d_terms, (cudaStream_t)stream));
+  return VLBM_OK;
+}
+
+int vlbm_d_ordered_mean(int64_t n, const double* d_terms, double* d_result, void* stream) {
+  CU(vlbm_impl::launch_ordered_mean(n, d_terms, d_result, (cudaStream_t)stream));
+  return VLBM_OK;
+}
+
+int vlbm_d_moments_planes(int M, int64_t n, const double* d_x, double* d_mean, double* d_std,
+                          void* stream) {
+  // one variable: x(m, c) = d_x[m * n + c]
+  if (M < 2) return set_error(VLBM_E_INVALID, "ensemble_moments: std requires at least 2 samples");
+  CU(vlbm_impl::launch_moments(M, n, d_x, n, d_mean, d_std, (cudaStream_t)stream));
+  return VLBM_OK;
+}
+
+}  // extern "C"

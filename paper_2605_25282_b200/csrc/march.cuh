@@ -1,0 +1,61 @@
+// march.cuh — device-side layout and control blocks of a batched VLBM march.
+//
+// HBM layout (one batch = S independent samples of one nx x ny grid):
+//   state[buf][s][20][ny][pitch]  f64, buf in {0,1} (ping-pong per sample):
+//       planes 0..3  u        (rho, mom_x, mom_y, E)       solver.hpp:589
+//       planes 4+4k+c pops[k] component c, k = 0..3         solver.hpp:590
+//   theta[s][ny][pitch]           f64 cell theta of the current step
+//   inlet[s][ny][4]               f64 inlet profile rows (host libm)
+//   ctl[s]                        per-sample control block (below)
+// No ghost cells are stored: the boundary ring is synthesised on load from
+// the interior (fill_ghosts semantics, solver.hpp:230-286).
+#pragma once
+#include <cstdint>
+
+#include "vlbm_device.cuh"
+
+namespace vlbm_dev {
+
+enum { BC_INLET = 0, BC_OUTFLOW = 1, BC_WALL = 2, BC_PERIODIC = 3 };
+enum { LIM_FIRST = 0, LIM_SECOND = 1, LIM_RLMP = 2 };
+enum { ST_RUNNING = 0, ST_DIVERGED = 2 };
+constexpr int kPlanes = 20;
+
+// Per-sample control block.  Written by k_sched (one thread per sample) and
+// by the advance epilogue (atomics on smax_bits / flags).
+struct SampleCtl {
+  double t;             // Simulation::time_
+  double dt;            // dt of the scheduled step
+  double a;             // a = dx / dt of the scheduled step
+  double smax_inlet;    // max signal speed over the inlet rows (constant)
+  unsigned long long smax_bits;  // max interior signal speed (bits; >0 doubles order as u64)
+  int bad_signal;       // some cell had a non-finite signal speed (rho<=0, p<=0, NaN)
+  int nonfinite;        // some component non-finite after the step
+  long long steps;      // Simulation::steps_
+  long long budget;     // steps still allowed in this call
+  int status;           // ST_RUNNING / ST_DIVERGED
+  int active;           // scheduled to step in the current iteration
+  int parity;           // buffer holding the current state
+  int pad;
+};
+
+struct MarchParams {
+  int nx, ny, pitch, S;
+  long long plane;          // ny * pitch
+  long long sample_stride;  // kPlanes * plane
+  double* buf0;
+  double* buf1;
+  double* theta;            // S * plane
+  const double* inlet;      // S * ny * 4
+  const double* face_tx;    // optional prescribed blending (S x ny x (nx+1))
+  const double* face_ty;    // (S x (ny+1) x nx)
+  SampleCtl* ctl;
+  int* n_active;
+  double dx, gamma, gm1, alpha, w, safety, kappa, rho_floor_coef, p_floor_coef;
+  double rho_ref, p_ref;
+  int bc[4];
+  int limiter;
+  int conservative;
+};
+
+}  // namespace vlbm_dev

@@ -1,0 +1,390 @@
+// post.cu — on-device W1/L1 post-processing of the empirical measures
+// (metrics.hpp:29-177), fp64, bit-identical to the reference.
+//
+//   k_restrict / k_restrict_var   restrict_field (metrics.hpp:29-49)
+//   k_strong_partials[_fused]     strong_error's per-sample sums (:69-80) in
+//                                 the reference's sequential order; the
+//                                 restriction of the fine sample is fused
+//   k_w1_*                        wasserstein1's per-cell term (:113-122):
+//                                 warp-per-cell bitonic sort of M <= 1024
+//                                 order-preserving 64-bit keys in registers,
+//                                 then the sequential sum over ranks
+//   k_ordered_mean                wasserstein1's storage-order acc (:122-124)
+//   k_moments                     ensemble_moments (:148-177)
+//
+// The serial chains (strong_error's num/den, W1's per-cell and per-field
+// sums) are evaluated in exactly the reference's order, one dependent DADD
+// per term, with the loads staged through shared memory by the other warps
+// so only the add latency is on the critical path.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "internal.h"
+
+namespace vlbm_dev {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// restrict_field: coarse(i,j) = 0.25 * (((f(2i,2j) + f(2i+1,2j)) + f(2i,2j+1)) + f(2i+1,2j+1))
+__device__ __forceinline__ double restrict_at(const double* f, int nxf, int i, int j) {
+  const double* r0 = f + (long long)(2 * j) * nxf + 2 * i;
+  const double* r1 = r0 + nxf;
+  const double sum = ((r0[0] + r0[1]) + r1[0]) + r1[1];
+  return sum * 0.25;
+}
+
+__global__ void k_restrict(int M, int nxc, int nyc, const double* fine, double* coarse) {
+  const long long nc = (long long)nxc * nyc, nf = 4 * nc;
+  const long long total = (long long)M * 4 * nc;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long mk = idx / nc;  // m * 4 + k
+    const long long c = idx - mk * nc;
+    const int j = (int)(c / nxc), i = (int)(c - (long long)j * nxc);
+    coarse[idx] = restrict_at(fine + mk * nf, 2 * nxc, i, j);
+  }
+}
+
+__global__ void k_restrict_var(int M, int nxc, int nyc, const double* fine, int var,
+                               double* out) {
+  const long long nc = (long long)nxc * nyc;
+  const long long total = (long long)M * nc;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long m = idx / nc;
+    const long long c = idx - m * nc;
+    const int j = (int)(c / nxc), i = (int)(c - (long long)j * nxc);
+    out[idx] = restrict_at(fine + (m * 4 + var) * 4 * nc, 2 * nxc, i, j);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// strong_error partials.  One CTA per sample; warps 1..3 stage (|a-b|, |b|)
+// for a chunk of cells into shared memory (double-buffered) while thread 0
+// runs the serial accumulation of the previous chunk in (cell, component)
+// order, exactly as metrics.hpp:71-80.
+constexpr int kSpChunk = 256;  // cells per chunk
+
+template <bool kFused>
+__global__ void __launch_bounds__(128) k_strong_partials(int M, long long n, int nxc,
+                                                         const double* a, const double* b,
+                                                         double* partials) {
+  __shared__ double sd[2][kSpChunk * 4];
+  __shared__ double sr[2][kSpChunk * 4];
+  const int m = blockIdx.x;
+  const double* A = a + (long long)m * 4 * n;
+  const double* B = b + (long long)m * 4 * n * (kFused ? 4 : 1);
+  const long long nchunks = (n + kSpChunk - 1) / kSpChunk;
+  auto stage = [&](long long ch, int buf, int t0, int nt) {
+    const long long c0 = ch * kSpChunk;
+    for (int q = t0; q < kSpChunk * 4; q += nt) {
+      const int cl = q >> 2, k = q & 3;
+      const long long c = c0 + cl;
+      if (c < n) {
+        double bv;
+        if (kFused) {
+          const int j = (int)(c / nxc), i = (int)(c - (long long)j * nxc);
+          bv = restrict_at(B + (long long)k * 4 * n, 2 * nxc, i, j);
+        } else {
+          bv = B[(long long)k * n + c];
+        }
+        const double av = A[(long long)k * n + c];
+        sd[buf][q] = fabs(av - bv);
+        sr[buf][q] = fabs(bv);
+      }
+    }
+  };
+  stage(0, 0, threadIdx.x, blockDim.x);
+  __syncthreads();
+  double num = 0.0, den = 0.0;
+  double cnum[4] = {0.0, 0.0, 0.0, 0.0}, cden[4] = {0.0, 0.0, 0.0, 0.0};
+  for (long long ch = 0; ch < nchunks; ++ch) {
+    const int buf = (int)(ch & 1);
+    if (threadIdx.x >= 32) {
+      if (ch + 1 < nchunks) stage(ch + 1, buf ^ 1, threadIdx.x - 32, blockDim.x - 32);
+    } else if (threadIdx.x == 0) {
+      const long long c0 = ch * kSpChunk;
+      const int nc = (int)((n - c0) < kSpChunk ? (n - c0) : kSpChunk);
+      for (int cl = 0; cl < nc; ++cl) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const double d = sd[buf][cl * 4 + k], r = sr[buf][cl * 4 + k];
+          num += d;
+          den += r;
+          cnum[k] += d;
+          cden[k] += r;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double* o = partials + (long long)m * 10;
+    o[0] = num;
+    o[1] = den;
+    for (int k = 0; k < 4; ++k) {
+      o[2 + k] = cnum[k];
+      o[6 + k] = cden[k];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// W1.  Order-preserving map of an IEEE double to an unsigned key.
+__device__ __forceinline__ unsigned long long dkey(double x) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double dval(unsigned long long k) {
+  const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double((long long)b);
+}
+
+// Bitonic sort of N = 32*R keys held by one warp, element e = lane*R + r.
+template <int R>
+__device__ __forceinline__ void warp_bitonic_sort(unsigned long long (&v)[R], int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32 * R; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= R) {
+        const int lm = j / R;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const unsigned long long o = __shfl_xor_sync(kFull, v[r], lm);
+          const int e = lane * R + r;
+          const bool take_min = (((e & j) == 0) == ((e & k) == 0));
+          const unsigned long long mn = o < v[r] ? o : v[r];
+          const unsigned long long mx = o < v[r] ? v[r] : o;
+          v[r] = take_min ? mn : mx;
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if ((r & j) == 0) {
+            const int r2 = r | j;
+            const int e = lane * R + r;
+            const bool asc = (e & k) == 0;
+            const unsigned long long x = v[r], y = v[r2];
+            const bool sw = asc ? (y < x) : (x < y);
+            v[r] = sw ? y : x;
+            v[r2] = sw ? x : y;
+          }
+        }
+      }
+    }
+  }
+}
+
+// Per-cell term: sum_m |a_(m) - b_(m)| over sorted ranks, sequential in m,
+// divided by M (metrics.hpp:118-122).  Loader functors return sample m's
+// value of the warp's cell.
+template <int R, class LA, class LB>
+__device__ __forceinline__ double w1_cell(int M, int lane, LA la, LB lb) {
+  unsigned long long ka[R], kb[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int m = r * 32 + lane;  // load slot: coalesced order; sorting is order-free
+    ka[r] = m < M ? dkey(la(m)) : ~0ull;
+    kb[r] = m < M ? dkey(lb(m)) : ~0ull;
+  }
+  warp_bitonic_sort<R>(ka, lane);
+  warp_bitonic_sort<R>(kb, lane);
+  // Ranks lane*R .. lane*R+R-1 live in this lane: the chain visits lanes in
+  // order, each adding its R terms, so the sum is strictly sequential in m.
+  double cell = 0.0;
+  for (int L = 0; L < 32; ++L) {
+    if (lane == L) {
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (L * R + r < M) cell += fabs(dval(ka[r]) - dval(kb[r]));
+    }
+    cell = __shfl_sync(kFull, cell, L);
+  }
+  return cell / static_cast<double>(M);
+}
+
+// Sample-major planes: value(m, c) = a[m * a_stride + c].
+template <int R>
+__global__ void __launch_bounds__(256) k_w1_planes(int M, long long n, const double* a,
+                                                   long long as, const double* b, long long bs,
+                                                   double* terms) {
+  const int lane = threadIdx.x & 31;
+  const long long c = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (c >= n) return;
+  const double t = w1_cell<R>(
+      M, lane, [&](int m) { return a[(long long)m * as + c]; },
+      [&](int m) { return b[(long long)m * bs + c]; });
+  if (lane == 0) terms[c] = t;
+}
+
+// Coarse planes vs restricted fine planes (restriction fused).
+template <int R>
+__global__ void __launch_bounds__(256) k_w1_restrict(int M, int nxc, int nyc, const double* a,
+                                                     long long as, const double* f,
+                                                     long long fs, double* terms) {
+  const int lane = threadIdx.x & 31;
+  const long long n = (long long)nxc * nyc;
+  const long long c = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (c >= n) return;
+  const int j = (int)(c / nxc), i = (int)(c - (long long)j * nxc);
+  const double t = w1_cell<R>(
+      M, lane, [&](int m) { return a[(long long)m * as + c]; },
+      [&](int m) { return restrict_at(f + (long long)m * fs, 2 * nxc, i, j); });
+  if (lane == 0) terms[c] = t;
+}
+
+// Cell-major columns (after the sample->cell re-shard): value(m, c) = a[c*M + m].
+template <int R>
+__global__ void __launch_bounds__(256) k_w1_cells(int M, long long n, const double* a,
+                                                  const double* b, double* terms) {
+  const int lane = threadIdx.x & 31;
+  const long long c = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (c >= n) return;
+  const double t = w1_cell<R>(
+      M, lane, [&](int m) { return a[c * M + m]; }, [&](int m) { return b[c * M + m]; });
+  if (lane == 0) terms[c] = t;
+}
+
+// acc = sum_c terms[c] in storage order; result = acc / n (metrics.hpp:112-124).
+constexpr int kOmChunk = 2048;
+__global__ void __launch_bounds__(256) k_ordered_mean(long long n, const double* terms,
+                                                     double* result) {
+  __shared__ double buf[2][kOmChunk];
+  const long long nchunks = (n + kOmChunk - 1) / kOmChunk;
+  auto stage = [&](long long ch, int bi, int t0, int nt) {
+    const long long c0 = ch * kOmChunk;
+    for (int q = t0; q < kOmChunk; q += nt)
+      if (c0 + q < n) buf[bi][q] = terms[c0 + q];
+  };
+  stage(0, 0, threadIdx.x, blockDim.x);
+  __syncthreads();
+  double acc = 0.0;
+  for (long long ch = 0; ch < nchunks; ++ch) {
+    const int bi = (int)(ch & 1);
+    if (threadIdx.x >= 32) {
+      if (ch + 1 < nchunks) stage(ch + 1, bi ^ 1, threadIdx.x - 32, blockDim.x - 32);
+    } else if (threadIdx.x == 0) {
+      const long long c0 = ch * kOmChunk;
+      const int nc = (int)((n - c0) < kOmChunk ? (n - c0) : kOmChunk);
+      for (int q = 0; q < nc; ++q) acc += buf[bi][q];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *result = acc / static_cast<double>(n);
+}
+
+// ensemble_moments per (component, cell) on sample-major blocks: x(m, q) =
+// x[m * stride + q], q over 4*n entries.
+__global__ void k_moments(int M, long long nq, const double* x, long long stride, double* mean,
+                          double* sd) {
+  const double inv_m = 1.0 / M;
+  const double inv_m1 = 1.0 / (M - 1.0);
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < nq;
+       q += (long long)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int m = 0; m < M; ++m) s += x[(long long)m * stride + q];
+    const double mu = s * inv_m;
+    double ss = 0.0;
+    for (int m = 0; m < M; ++m) {
+      const double d = x[(long long)m * stride + q] - mu;
+      ss += d * d;
+    }
+    mean[q] = mu;
+    sd[q] = sqrt(ss * inv_m1);
+  }
+}
+
+}  // namespace vlbm_dev
+
+namespace vlbm_impl {
+using namespace vlbm_dev;
+
+static int grid_for(long long total, int threads = 256, int cap = 148 * 32) {
+  long long b = (total + threads - 1) / threads;
+  if (b < 1) b = 1;
+  return (int)(b > cap ? cap : b);
+}
+
+cudaError_t launch_restrict(int M, int nxc, int nyc, const double* fine, double* coarse,
+                            cudaStream_t st) {
+  k_restrict<<<grid_for((long long)M * 4 * nxc * nyc), 256, 0, st>>>(M, nxc, nyc, fine, coarse);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_restrict_var(int M, int nxc, int nyc, const double* fine, int var, double* out,
+                                cudaStream_t st) {
+  k_restrict_var<<<grid_for((long long)M * nxc * nyc), 256, 0, st>>>(M, nxc, nyc, fine, var, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_strong_partials(int M, int64_t n, const double* a, const double* b,
+                                   double* partials, cudaStream_t st) {
+  k_strong_partials<false><<<M, 128, 0, st>>>(M, n, 0, a, b, partials);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_strong_partials_fused(int M, int nxc, int nyc, const double* coarse,
+                                         const double* fine, double* partials, cudaStream_t st) {
+  k_strong_partials<true><<<M, 128, 0, st>>>(M, (long long)nxc * nyc, nxc, coarse, fine,
+                                             partials);
+  return cudaGetLastError();
+}
+
+template <template <int> class K>
+struct Dispatch;
+
+#define W1_DISPATCH(KERNEL, M, grid, st, ...)                                   \
+  do {                                                                          \
+    if ((M) <= 32)                                                              \
+      KERNEL<1><<<grid, 256, 0, st>>>(__VA_ARGS__);                             \
+    else if ((M) <= 64)                                                         \
+      KERNEL<2><<<grid, 256, 0, st>>>(__VA_ARGS__);                             \
+    else if ((M) <= 128)                                                        \
+      KERNEL<4><<<grid, 256, 0, st>>>(__VA_ARGS__);                             \
+    else if ((M) <= 256)                                                        \
+      KERNEL<8><<<grid, 256, 0, st>>>(__VA_ARGS__);                             \
+    else if ((M) <= 512)                                                        \
+      KERNEL<16><<<grid, 256, 0, st>>>(__VA_ARGS__);                            \
+    else                                                                        \
+      KERNEL<32><<<grid, 256, 0, st>>>(__VA_ARGS__);                            \
+  } while (0)
+
+cudaError_t launch_w1_planes(int M, int64_t n, const double* a, int64_t as, const double* b,
+                             int64_t bs, double* terms, cudaStream_t st) {
+  if (M < 1 || M > 1024) return cudaErrorInvalidValue;
+  const int grid = (int)((n + 7) / 8);
+  W1_DISPATCH(k_w1_planes, M, grid, st, M, n, a, as, b, bs, terms);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_w1_restrict(int M, int nxc, int nyc, const double* a, int64_t as,
+                               const double* f, int64_t fs, double* terms, cudaStream_t st) {
+  if (M < 1 || M > 1024) return cudaErrorInvalidValue;
+  const long long n = (long long)nxc * nyc;
+  const int grid = (int)((n + 7) / 8);
+  W1_DISPATCH(k_w1_restrict, M, grid, st, M, nxc, nyc, a, as, f, fs, terms);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_w1_cells(int M, int64_t n, const double* a, const double* b, double* terms,
+                            cudaStream_t st) {
+  if (M < 1 || M > 1024) return cudaErrorInvalidValue;
+  const int grid = (int)((n + 7) / 8);
+  W1_DISPATCH(k_w1_cells, M, grid, st, M, n, a, b, terms);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ordered_mean(int64_t n, const double* terms, double* result, cudaStream_t st) {
+  k_ordered_mean<<<1, 256, 0, st>>>(n, terms, result);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_moments(int M, int64_t nq, const double* x, int64_t stride, double* mean,
+                           double* sd, cudaStream_t st) {
+  k_moments<<<grid_for(nq), 256, 0, st>>>(M, nq, x, stride, mean, sd);
+  return cudaGetLastError();
+}
+
+}  // namespace vlbm_impl

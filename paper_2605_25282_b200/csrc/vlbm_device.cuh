@@ -1,0 +1,93 @@
+// vlbm_device.cuh — fp64 device primitives of the VLBM march, bit-identical to
+// the reference's host arithmetic.
+//
+// Bit-parity rules (SURVEY.md §7.3, §8a bit-parity notes):
+//  * compiled with --fmad=false: every a*b+c below is a separate DMUL + DADD,
+//    as in the reference's x86-64 build (no FMA contraction);
+//  * '/' and sqrt are IEEE round-to-nearest (div.rn.f64 / sqrt.rn.f64);
+//  * association order is the reference's, term by term;
+//  * std::min/std::max semantics: ties (and +-0) keep the FIRST argument.
+#pragma once
+#include <cstdint>
+
+namespace vlbm_dev {
+
+struct cs {  // ConservedState, euler.hpp:16-46 (rho, mom_x, mom_y, energy)
+  double r, mx, my, e;
+};
+
+__device__ __forceinline__ cs add(const cs& a, const cs& b) {
+  return {a.r + b.r, a.mx + b.mx, a.my + b.my, a.e + b.e};
+}
+__device__ __forceinline__ cs sub(const cs& a, const cs& b) {
+  return {a.r - b.r, a.mx - b.mx, a.my - b.my, a.e - b.e};
+}
+// operator*(double s, ConservedState a) == a *= s, euler.hpp:39-50
+__device__ __forceinline__ cs scale(double s, const cs& a) {
+  return {a.r * s, a.mx * s, a.my * s, a.e * s};
+}
+__device__ __forceinline__ double smin(double a, double b) { return (b < a) ? b : a; }
+__device__ __forceinline__ double smax(double a, double b) { return (a < b) ? b : a; }
+
+// pressure, euler.hpp:62-65 — no clamp.
+__device__ __forceinline__ double pressure(const cs& u, double gm1) {
+  const double kinetic = 0.5 * (u.mx * u.mx + u.my * u.my) / u.r;
+  return gm1 * (u.e - kinetic);
+}
+
+// flux_x / flux_y, euler.hpp:86-97.
+__device__ __forceinline__ cs flux_x(const cs& u, double gm1) {
+  const double v1 = u.mx / u.r;
+  const double p = pressure(u, gm1);
+  return {u.mx, u.mx * v1 + p, u.my * v1, (u.e + p) * v1};
+}
+__device__ __forceinline__ cs flux_y(const cs& u, double gm1) {
+  const double v2 = u.my / u.r;
+  const double p = pressure(u, gm1);
+  return {u.my, u.mx * v2, u.my * v2 + p, (u.e + p) * v2};
+}
+
+// maxwellians, lattice.hpp:43-55, split by direction: M1/M2 need only f,
+// M3/M4 only g (each M_k is computed exactly as the reference computes it).
+// w = 0.25*(1-alpha) and inv2a = 0.5/a are passed in (identical values).
+__device__ __forceinline__ void maxw_x(const cs& u, double w, double inv2a, double gm1, cs& m0,
+                                       cs& m1) {
+  const cs f = flux_x(u, gm1);
+  const cs wu = scale(w, u);
+  const cs fa = scale(inv2a, f);
+  m0 = add(wu, fa);
+  m1 = sub(wu, fa);
+}
+__device__ __forceinline__ void maxw_y(const cs& u, double w, double inv2a, double gm1, cs& m2,
+                                       cs& m3) {
+  const cs g = flux_y(u, gm1);
+  const cs wu = scale(w, u);
+  const cs ga = scale(inv2a, g);
+  m2 = add(wu, ga);
+  m3 = sub(wu, ga);
+}
+__device__ __forceinline__ cs maxw_k(const cs& u, int k, double w, double inv2a, double gm1) {
+  cs a, b;
+  if (k < 2) {
+    maxw_x(u, w, inv2a, gm1, a, b);
+  } else {
+    maxw_y(u, w, inv2a, gm1, a, b);
+  }
+  return (k & 1) ? b : a;
+}
+
+// signal_speed, solver.hpp:203-209.  Returns NaN for rho<=0 or p<=0.
+__device__ __forceinline__ double signal_speed(const cs& u, double gamma, double gm1,
+                                               int conservative) {
+  const double p = pressure(u, gm1);
+  if (!(u.r > 0.0) || !(p > 0.0)) return __longlong_as_double(0x7ff8000000000000ll);
+  const double c = sqrt(gamma * p / u.r);
+  if (conservative) return hypot(u.mx, u.my) / u.r + c;
+  return smax(fabs(u.mx), fabs(u.my)) / u.r + c;
+}
+
+__device__ __forceinline__ bool finite4(const cs& u) {
+  return isfinite(u.r) && isfinite(u.mx) && isfinite(u.my) && isfinite(u.e);
+}
+
+}  // namespace vlbm_dev

@@ -1,0 +1,269 @@
+"""GPU parity of the batched VLBM march against the CPU oracle (-m gpu).
+
+Every comparison is BIT-EXACT (uint64 views, so +-0 and NaN payloads count):
+the limiter's discrete decisions amplify one ulp to O(1) within ~50 steps
+(SURVEY.md §0 fact 4), so anything short of bit identity is a failure.  The
+oracle (oracle/vlbm_oracle.c) is itself pinned bit-for-bit to the reference
+(tests/test_oracle_pin.py).
+"""
+import numpy as np
+import pytest
+
+from oracle.oracle import (INLET, OUTFLOW, PERIODIC, WALL, FIRST_ORDER, SECOND_ORDER, RLMP,
+                           make_grid, make_params, make_pert)
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float64).view(np.uint64)
+
+
+def assert_bitwise(got, want, what):
+    if not np.array_equal(bits(got), bits(want)):
+        d = np.abs(np.asarray(got) - np.asarray(want))
+        bad = np.argwhere(bits(got) != bits(want))
+        raise AssertionError(f"{what}: {len(bad)} entries differ, first at {bad[0].tolist()}, "
+                             f"max |d| = {np.nanmax(d):.3e}")
+
+
+# ---- config 1: 200x40, M=8, 200 steps of step(suggest_dt()) -----------------
+
+def test_config1_bitwise_per_step(vlbm, vo):
+    """BASELINE configs[0]: every sample's u, pops and cell theta bit-identical
+    to the oracle after steps 1, 2, 5, 20, 50, 100 and 200."""
+    g = vlbm.Grid(200, 40)
+    M = 8
+    sim = vlbm.BatchSimulation.jet(g, n_samples=M, base_seed=42)
+    refs = [vo.jet_sim(make_grid(200, 40), make_params(), make_pert(), 42, m) for m in range(M)]
+    done = 0
+    for target in (1, 2, 5, 20, 50, 100, 200):
+        sim.step(target - done)
+        for r in refs:
+            for _ in range(target - done):
+                r.step(r.suggest_dt())
+        done = target
+        t, steps, status = sim.scalars()
+        for m, r in enumerate(refs):
+            assert steps[m] == target and status[m] == 0
+            assert bits(t[m]) == bits(r.time), (m, t[m], r.time)
+            u, p = r.get(pops=True)
+            assert_bitwise(sim.state(m), u, f"u sample {m} step {target}")
+            assert_bitwise(sim.populations(m), p, f"pops sample {m} step {target}")
+    # cell theta of the last step (oracle keeps it after the step)
+    for m, r in enumerate(refs):
+        assert_bitwise(sim.theta_cell(m), r.theta_cell(), f"theta sample {m}")
+
+
+def test_run_samples_matches_run_sample(vlbm, vo):
+    """run_samples == run_sample for every snapshot of 3 samples on the smoke
+    grid 125x25 to t_end = 0.003 (times, diverged flags, steps, fields)."""
+    times = [0.0, 0.00075, 0.0015, 0.00225, 0.003]
+    g = vlbm.Grid(125, 25)
+    res = vlbm.run_samples(g, vlbm.LatticeParams(), vlbm.GasParams(), vlbm.PerturbationParams(),
+                           42, 0, 3, 0.02, times)
+    for m in range(3):
+        want = vo.run_sample(make_grid(125, 25), make_params(), make_pert(), 42, m, times)
+        r = res[m]
+        assert r.steps == want["steps"] and r.admissible == want["admissible"]
+        for ti in range(len(times)):
+            s = r.snapshots[ti]
+            assert s.time == want["time"][ti] and s.diverged == want["diverged"][ti]
+            assert s.sample_seed == want["seed"]
+            assert_bitwise(s.data, want["fields"][ti], f"snapshot m={m} t={ti}")
+
+
+def test_samples_not_in_lockstep(vlbm, vo):
+    """Samples keep their own dt: a batch that starts at m0=5 reproduces the
+    oracle's samples 5..8 (different step counts to the same target)."""
+    g = vlbm.Grid(100, 20)
+    sim = vlbm.BatchSimulation.jet(g, n_samples=4, base_seed=7, m0=5)
+    sim.run_to(0.0004)
+    t, steps, status = sim.scalars()
+    for s in range(4):
+        r = vo.jet_sim(make_grid(100, 20), make_params(), make_pert(), 7, 5 + s)
+        n = 0
+        while r.time < 0.0004 - 1e-12:
+            r.step(min(r.suggest_dt(), 0.0004 - r.time))
+            n += 1
+        assert steps[s] == n
+        assert bits(t[s]) == bits(r.time)
+        assert_bitwise(sim.state(s), r.get(), f"sample {5 + s}")
+
+
+# ---- boundary variants and limiter modes -------------------------------------
+
+def smooth_field(nx, ny, x_max, gamma=1.4):
+    """test_solver.cpp:31-48's smooth periodic field (conserved variables)."""
+    dx = x_max / nx
+    ly = 0.5
+    x = (np.arange(nx) + 0.5) * dx
+    y = -0.25 + (np.arange(ny) + 0.5) * dx
+    X, Y = np.meshgrid(x, y)
+    rho = 1.0 + 0.3 * np.sin(2 * np.pi * X / x_max) * np.cos(2 * np.pi * (Y + 0.25) / ly)
+    v1 = 0.2 * np.cos(2 * np.pi * X / x_max)
+    v2 = 0.1 * np.sin(2 * np.pi * (Y + 0.25) / ly)
+    p = 1.0 + 0.2 * np.cos(2 * np.pi * X / x_max)
+    E = p / (gamma - 1.0) + 0.5 * rho * (v1 * v1 + v2 * v2)
+    return np.stack([rho, rho * v1, rho * v2, E])
+
+
+BC_CASES = {
+    "all_periodic": ((PERIODIC, PERIODIC, PERIODIC, PERIODIC), 32, 32),
+    "periodic_x_wall_y": ((PERIODIC, PERIODIC, WALL, WALL), 32, 16),
+    "outflow_x_periodic_y": ((OUTFLOW, OUTFLOW, PERIODIC, PERIODIC), 40, 8),
+    "outflow_x_wall_y": ((OUTFLOW, OUTFLOW, WALL, WALL), 24, 12),
+}
+
+
+@pytest.mark.parametrize("case", list(BC_CASES))
+@pytest.mark.parametrize("limiter", [RLMP, FIRST_ORDER, SECOND_ORDER])
+def test_boundary_variants_bitwise(vlbm, vo, case, limiter):
+    bc, nx, ny = BC_CASES[case]
+    x_max = 0.5 * nx / ny
+    init = smooth_field(nx, ny, x_max)
+    # a spike so the limiter engages
+    init[0, ny // 2, nx // 3] *= 3.0
+    init[3, ny // 2, nx // 3] *= 3.0
+    gamma = 1.4
+    g = vlbm.Grid(nx, ny, x_max)
+    lat = vlbm.LatticeParams(limiter=vlbm.Limiter(limiter))
+    bcs = vlbm.Boundaries(*[vlbm.BcType(b) for b in bc])
+    sim = vlbm.BatchSimulation(g, lat, vlbm.GasParams(gamma), bcs, init)
+    r = vo.sim(make_grid(nx, ny, x_max), make_params(gamma=gamma, limiter=limiter, bc=bc), init)
+    for n in (1, 4, 15):
+        sim.step(n)
+        for _ in range(n):
+            r.step(r.suggest_dt())
+        u, p = r.get(pops=True)
+        assert_bitwise(sim.state(0), u, f"{case} u")
+        assert_bitwise(sim.populations(0), p, f"{case} pops")
+
+
+def test_inlet_generic_fields_and_alpha(vlbm, vo):
+    """Generic construction with inlet rows and alpha = 0.25 (M5 = alpha u)."""
+    nx, ny = 60, 12
+    g = vlbm.Grid(nx, ny)
+    pp = make_pert()
+    seed, yc, zc = vo.draw_coefficients(3, 1, 10)
+    rows = vo.inlet_rows(make_grid(nx, ny), yc, zc, pp)
+    init = vo.initial_field(make_grid(nx, ny), yc, zc, pp, strip=0.1)
+    lat = vlbm.LatticeParams(alpha=0.25)
+    sim = vlbm.BatchSimulation(g, lat, vlbm.GasParams(), vlbm.Boundaries(), init, rows)
+    r = vo.sim(make_grid(nx, ny), make_params(alpha=0.25), init, rows)
+    sim.step(30)
+    for _ in range(30):
+        r.step(r.suggest_dt())
+    u, p = r.get(pops=True)
+    assert_bitwise(sim.state(0), u, "alpha u")
+    assert_bitwise(sim.populations(0), p, "alpha pops")
+
+
+def test_fixed_dt_steps(vlbm, vo):
+    nx, ny = 40, 8
+    init = smooth_field(nx, ny, 0.5 * nx / ny)
+    g = vlbm.Grid(nx, ny, 0.5 * nx / ny)
+    bcs = vlbm.Boundaries(*[vlbm.BcType.Periodic] * 4)
+    sim = vlbm.BatchSimulation(g, vlbm.LatticeParams(), vlbm.GasParams(1.4), bcs, init)
+    r = vo.sim(make_grid(nx, ny, 0.5 * nx / ny), make_params(gamma=1.4, bc=(3, 3, 3, 3)), init)
+    dt = 0.7 * r.suggest_dt()
+    sim.step(10, dt=dt)
+    for _ in range(10):
+        r.step(dt)
+    assert_bitwise(sim.state(0), r.get(), "fixed dt")
+
+
+def test_step_with_blending_random(vlbm, vo):
+    """step_with_blending (solver.hpp:173-181) with random interface thetas."""
+    nx, ny = 16, 16
+    x_max = 0.5
+    init = smooth_field(nx, ny, x_max)
+    g = vlbm.Grid(nx, ny, x_max)
+    bcs = vlbm.Boundaries(*[vlbm.BcType.Periodic] * 4)
+    sim = vlbm.BatchSimulation(g, vlbm.LatticeParams(), vlbm.GasParams(1.4), bcs, init)
+    r = vo.sim(make_grid(nx, ny, x_max), make_params(gamma=1.4, bc=(3, 3, 3, 3)), init)
+    rng = np.random.default_rng(5)
+    for _ in range(5):
+        tx = rng.random((ny, nx + 1))
+        ty = rng.random((ny + 1, nx))
+        tx[:, nx] = tx[:, 0]
+        ty[ny, :] = ty[0, :]
+        dt = r.suggest_dt()
+        sim.step_with_blending(tx, ty)
+        r.step_with_blending(dt, tx, ty)
+    assert_bitwise(sim.state(0), r.get(), "blended")
+
+
+# ---- reference solver invariants, replayed on the kernel (test_solver.cpp) ----
+
+def test_uniform_state_fixed_point(vlbm):
+    """test_solver.cpp:75-95: a uniform state is invariant for any blending."""
+    gamma = 1.4
+    rho, v1, v2, p = 1.3, 0.4, -0.2, 0.9
+    u0 = np.array([rho, rho * v1, rho * v2, p / (gamma - 1) + 0.5 * rho * (v1 * v1 + v2 * v2)])
+    nx = ny = 16
+    init = np.broadcast_to(u0[:, None, None], (4, ny, nx)).copy()
+    g = vlbm.Grid(nx, ny, 0.5)
+    bcs = vlbm.Boundaries(*[vlbm.BcType.Periodic] * 4)
+    for alpha in (0.0, 0.25):
+        sim = vlbm.BatchSimulation(g, vlbm.LatticeParams(alpha=alpha), vlbm.GasParams(gamma), bcs,
+                                   init)
+        rng = np.random.default_rng(5)
+        for _ in range(10):
+            tx = rng.random((ny, nx + 1))
+            ty = rng.random((ny + 1, nx))
+            tx[:, nx] = tx[:, 0]
+            ty[ny, :] = ty[0, :]
+            sim.step_with_blending(tx, ty)
+        np.testing.assert_allclose(sim.state(0), init, rtol=1e-13)
+
+
+def test_periodic_conservation(vlbm):
+    """test_solver.cpp:97-112: periodic RLMP run conserves all four totals."""
+    nx = ny = 32
+    init = smooth_field(nx, ny, 0.5)
+    g = vlbm.Grid(nx, ny, 0.5)
+    bcs = vlbm.Boundaries(*[vlbm.BcType.Periodic] * 4)
+    sim = vlbm.BatchSimulation(g, vlbm.LatticeParams(), vlbm.GasParams(1.4), bcs, init)
+    before = init.reshape(4, -1).sum(1)
+    sim.step(50)
+    after = sim.state(0).reshape(4, -1).sum(1)
+    scale = np.maximum(np.abs(before), 1.0)
+    assert np.all(np.abs(after - before) / scale <= 1e-12)
+
+
+def test_mirror_symmetry_unperturbed_jet(vlbm):
+    """test_solver.cpp:228-263: amplitude 0 jet stays mirror symmetric."""
+    g = vlbm.Grid(100, 20)
+    pp = vlbm.PerturbationParams(amplitude=0.0)
+    res = vlbm.run_samples(g, vlbm.LatticeParams(), vlbm.GasParams(), pp, 1, 0, 1, 0.0, [0.0005])
+    s = res[0].snapshots[0].data
+    assert res[0].admissible
+    scale = np.abs(s).reshape(4, -1).max(1)
+    m = s[:, ::-1, :]
+    assert np.all(np.abs(s[0] - m[0]) <= 1e-10 * scale[0])
+    assert np.all(np.abs(s[1] - m[1]) <= 1e-10 * scale[1])
+    assert np.all(np.abs(s[2] + m[2]) <= 1e-10 * scale[1])
+    assert np.all(np.abs(s[3] - m[3]) <= 1e-10 * scale[3])
+    assert np.abs(s[0] - 0.5).sum() > 1.0
+
+
+def test_divergence_flags_like_run_sample(vlbm, vo):
+    """A blow-up (tiny safety factor, no limiter) is an outcome, not an error:
+    the sample stops, later snapshots are placeholders with the sample's own
+    time, exactly as run_sample (solver.hpp:645-666)."""
+    times = [0.0, 0.0002, 0.0004]
+    g = vlbm.Grid(60, 12)
+    lat = vlbm.LatticeParams(limiter=vlbm.Limiter.SecondOrder, safety=1.0)
+    res = vlbm.run_samples(g, lat, vlbm.GasParams(), vlbm.PerturbationParams(), 42, 0, 2, 0.02,
+                           times)
+    for m in range(2):
+        want = vo.run_sample(make_grid(60, 12), make_params(limiter=SECOND_ORDER, safety=1.0),
+                             make_pert(), 42, m, times)
+        assert res[m].admissible == want["admissible"]
+        assert res[m].steps == want["steps"]
+        for ti in range(3):
+            s = res[m].snapshots[ti]
+            assert bits(s.time) == bits(want["time"][ti])
+            assert s.diverged == want["diverged"][ti]
+            assert_bitwise(s.data, want["fields"][ti], f"diverging sample {m} t{ti}")
