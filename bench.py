@@ -1,0 +1,367 @@
+#!/usr/bin/env python
+"""bench.py — the VLBM hot path on B200, one JSON line on rank 0.
+
+Workload (N=1): BASELINE.json configs[1], the Mach-2000 jet at 1000x200 with
+M=64 Monte-Carlo samples per GPU (weak scaling: rank r marches samples
+r*64 .. r*64+63, no data-path collective).  One bench "step" = one VLBM time
+step of every sample of the batch (each sample with its own adaptive dt, as
+run_sample marches it).  Metric: sample-cell updates/s (whole job).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Timing: W untimed steps, then EXACTLY K steps bracketed by barrier +
+synchronize, CUDA events on the library's stream, max over ranks.  The state
+(64 x 20 planes x 200k cells x 8 B x 2 buffers = 4.1 GB) is far larger than
+L2 (126 MB): "inputs larger than L2".
+
+Extra keys: e2e (the same march through the public API from host buffers,
+H2D of the initial fields and D2H of the final fields inside the timed
+region), roofline (dominant kernel, live CUDA events), cpu_baseline (the
+reference CPU path on this host), clocks (nvidia-smi during the timed
+region), postproc (W1/L1 on BASELINE configs[3]'s synthetic ensembles).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+NX, NY, M_PER_GPU = 1000, 200, 64
+BYTES_PER_UPDATE = 320      # read u(4)+pops(16) f64, write the same
+THETA_BYTES_PER_CELL = 168  # k_theta: read u + pops (160 B), write theta (8 B)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = sorted({n for r in self.rows for n, v in zip(self.NAMES, r[2:])
+                          if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_reference(args, n_gpus, threads=None, seconds=15.0):
+    """The reference CPU march (oracle/_ref = the unmodified reference
+    headers) on this host's cores: one sample per thread, run_ensemble-style
+    task pool, file I/O excluded; a bounded sample of the same workload
+    (1000x200 jet samples, the first `steps` VLBM steps of each)."""
+    from oracle import oracle
+    threads = threads or os.cpu_count() or 1
+    kind = "reference" if oracle.available("ref") else "port"
+    o = oracle.Oracle("ref" if kind == "reference" else "vo")
+    g, p, pp = oracle.make_grid(NX, NY), oracle.make_params(), oracle.make_pert()
+    if kind == "reference":
+        # calibrate: ~1.4e6 updates/s/core measured in the survey; aim for `seconds`
+        n_samples = min(M_PER_GPU, threads)
+        steps = max(2, int(seconds * 1.4e6 * min(threads, n_samples) / (n_samples * NX * NY)))
+        sec, upd = o.march_timed(g, p, pp, 42, 0, n_samples, steps, 0.0, 0.02, threads)
+    else:
+        import concurrent.futures as cf
+        n_samples, steps = min(M_PER_GPU, threads), 5
+
+        def one(m):
+            s = o.jet_sim(g, p, pp, 42, m)
+            for _ in range(steps):
+                s.step(s.suggest_dt())
+            return steps * NX * NY
+
+        t0 = time.perf_counter()
+        with cf.ThreadPoolExecutor(threads) as ex:
+            upd = sum(ex.map(one, range(n_samples)))
+        sec = time.perf_counter() - t0
+    used = min(threads, n_samples)
+    return {"value": upd / sec, "unit": "sample-cell-updates/s", "cores": used, "kind": kind,
+            "sample": f"{n_samples} jet samples x first {steps} steps at {NX}x{NY} "
+                      f"({upd:.3g} updates, {sec:.1f} s wall, {used} threads)"}
+
+
+def postproc_bench(torch, dev, M=1000, nxc=2000, nyc=400, reps=3):
+    """BASELINE configs[3]: W1 + L1 of M synthetic log-normal density
+    ensembles (mu = -sigma^2/2, sigma = 0.5, so E[rho] = 1), coarse
+    nxc x nyc vs the restriction of fine 2nxc x 2nyc, on device.  Other
+    components are identically zero, so the density-only L1 equals the
+    reference's 4-component strong_error bit-for-bit."""
+    from paper_2605_25282_b200 import post
+    nc, nf = nxc * nyc, 4 * nxc * nyc
+    need = 8 * M * (nc + nf) + (1 << 30)
+    free, _ = torch.cuda.mem_get_info(dev)
+    if need > free:
+        M = max(32, int(M * free / need) // 32 * 32)
+    gen = torch.Generator(device=f"cuda:{dev}")
+    coarse = torch.empty((M, nyc, nxc), dtype=torch.float64, device=f"cuda:{dev}")
+    fine = torch.empty((M, 2 * nyc, 2 * nxc), dtype=torch.float64, device=f"cuda:{dev}")
+    gen.manual_seed(1)
+    coarse.normal_(-0.125, 0.5, generator=gen).exp_()
+    gen.manual_seed(2)
+    fine.normal_(-0.125, 0.5, generator=gen).exp_()
+    terms = torch.empty(nc, dtype=torch.float64, device=coarse.device)
+    res = torch.empty(1, dtype=torch.float64, device=coarse.device)
+    part = torch.empty((M, 10), dtype=torch.float64, device=coarse.device)
+    post.w1_cell_terms(torch, coarse, fine, terms)
+    post.ordered_mean(torch, terms, res)
+    post.strong_partials(torch, coarse, fine, part)
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    w1_ms, mean_ms, l1_ms = [], [], []
+    for _ in range(reps):
+        ev[0].record()
+        post.w1_cell_terms(torch, coarse, fine, terms)
+        ev[1].record()
+        post.ordered_mean(torch, terms, res)
+        ev[2].record()
+        post.strong_partials(torch, coarse, fine, part)
+        ev[3].record()
+        torch.cuda.synchronize()
+        w1_ms.append(ev[0].elapsed_time(ev[1]))
+        mean_ms.append(ev[1].elapsed_time(ev[2]))
+        l1_ms.append(ev[2].elapsed_time(ev[3]))
+    w1 = float(res.item())
+    es = post.strong_finish(part.cpu().numpy())
+    w1t = statistics.median(w1_ms) + statistics.median(mean_ms)
+    l1t = statistics.median(l1_ms)
+    hbm, src = peaks()
+    w1_bytes = 40.0 * M * nc  # M coarse + 4M fine values per coarse cell
+    l1_bytes = 40.0 * M * nc
+    del coarse, fine
+    torch.cuda.empty_cache()
+    return {
+        "workload": f"C4 synthetic log-normal rho, M={M}, coarse {nxc}x{nyc} vs restricted "
+                    f"fine {2 * nxc}x{2 * nyc}",
+        "w1_cells_per_s": nc / (w1t * 1e-3), "w1_ms": w1t,
+        "w1_kernel_ms": statistics.median(w1_ms), "ordered_mean_ms": statistics.median(mean_ms),
+        "w1_values_sorted_per_s": 2 * M * nc / (statistics.median(w1_ms) * 1e-3),
+        "w1_roofline": {"bound": "hbm", "achieved": w1_bytes / (statistics.median(w1_ms) * 1e-3)
+                        / 1e9, "peak": hbm, "unit": "GB/s",
+                        "frac": w1_bytes / (statistics.median(w1_ms) * 1e-3) / 1e9 / hbm,
+                        "bytes_per_cell": 40 * M, "peak_source": src},
+        "l1_sample_cells_per_s": M * nc / (l1t * 1e-3), "l1_ms": l1t,
+        "l1_roofline_frac": l1_bytes / (l1t * 1e-3) / 1e9 / hbm,
+        "W1": w1, "E_strong": es,
+    }
+
+
+def run_reference_arm(args):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    cb = cpu_reference(args, ws)
+    line = {"impl": "reference", "metric": "VLBM sample-cell updates/s",
+            "value": cb["value"], "unit": "sample-cell-updates/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"C2 jet {NX}x{NY}, M={M_PER_GPU}/GPU, RLMP, fp64",
+                       "nx": NX, "ny": NY, "samples_per_gpu": M_PER_GPU},
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "sample-cell-updates/s",
+                    "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--samples", type=int, default=M_PER_GPU)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-postproc", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import numpy as np
+    import torch
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2605_25282_b200 as v
+
+    M = args.samples
+    g = v.Grid(NX, NY)
+    lat, gas, pp = v.LatticeParams(), v.GasParams(), v.PerturbationParams()
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    # ---- device-resident march ----
+    sim = v.BatchSimulation.jet(g, lat, gas, pp, base_seed=42, m0=rank * M, n_samples=M,
+                                device=local)
+    stream = torch.cuda.ExternalStream(sim.stream(), device=torch.device("cuda", local))
+    sim.step(args.warmup)
+    sim.set_timing(True)
+    st0 = sim.stats()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        sim.step(args.steps)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = ev0.elapsed_time(ev1)
+    st1 = sim.stats()
+    updates = st1["cell_updates"] - st0["cell_updates"]
+    launches = st1["launches"] - st0["launches"]
+    n_theta = args.steps  # one k_theta launch per step (RLMP)
+    theta_ms = st1["ms_theta"] / max(n_theta, 1)
+    adv_ms = st1["ms_advance"] / max(args.steps, 1)
+    sched_ms = st1["ms_sched"] / max(args.steps, 1)
+    t_max = ms
+    upd_total = updates
+    if ws > 1:
+        tt = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_max = float(tt.item())
+        uu = torch.tensor([updates], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(uu)
+        upd_total = float(uu.item())
+    value = upd_total / (t_max * 1e-3)
+    sim.close()
+
+    # ---- e2e through the public API from host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        # The user's call sequence: build the batch from the seeds (host IC
+        # through libm, H2D of the initial fields and inlet rows), march K
+        # steps, read every sample's final field back to host memory.
+        out = torch.empty((M, 4, NY, NX), dtype=torch.float64).pin_memory().numpy()
+        barrier()
+        t0 = time.perf_counter()
+        e = v.BatchSimulation.jet(g, lat, gas, pp, base_seed=42, m0=rank * M, n_samples=M,
+                                  device=local)
+        e.step(args.steps)
+        v.vlbm._check(v.lib().vlbm_batch_get_fields(e._h, v.vlbm._dp(out)))
+        t1 = time.perf_counter()
+        barrier()
+        st = e.stats()
+        e.close()
+        et = t1 - t0
+        if ws > 1:
+            tt = torch.tensor([et], device="cuda", dtype=torch.float64)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            et = float(tt.item())
+        h2d = M * (4 * NX * NY + 4 * NY) * 8
+        e2e = {"value": st["cell_updates"] * ws / et, "unit": "sample-cell-updates/s",
+               "h2d_bytes_per_step": int(h2d / args.steps),
+               "d2h_bytes_per_step": int(out.nbytes / args.steps),
+               "note": "BatchSimulation.jet (host IC + H2D) + K steps + D2H of all fields"}
+
+    # ---- post-processing (BASELINE configs[3]) ----
+    post = None
+    if not args.no_postproc and rank == 0:
+        post = postproc_bench(torch, local)
+
+    if rank == 0:
+        hbm, src = peaks()
+        cells_per_launch = M * NX * NY
+        achieved = THETA_BYTES_PER_CELL * cells_per_launch / (theta_ms * 1e-3) / 1e9
+        step_gbs = BYTES_PER_UPDATE * (updates / (ms * 1e-3)) / 1e9
+        line = {
+            "metric": "VLBM sample-cell updates/s (GLUPS) & % HBM roofline; W1 post-proc cells/s",
+            "value": value, "unit": "sample-cell-updates/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (jet IC from splitmix64 seeds, base_seed 42)",
+            "config": {"workload": f"C2 jet {NX}x{NY}, M={M}/GPU, RLMP, fp64, steps "
+                                   f"{args.warmup}..{args.warmup + args.steps} of each sample",
+                       "nx": NX, "ny": NY, "samples_per_gpu": M, "parallelism": f"samples/{ws}",
+                       "l2": "inputs larger than L2 (4.1 GB state per GPU)"},
+            "glups": value / 1e9,
+            "gpu_launches": launches,
+            "roofline": {"bound": "hbm", "kernel": "k_theta", "achieved": achieved, "peak": hbm,
+                         "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                         "peak_source": src,
+                         "bytes_per_cell": THETA_BYTES_PER_CELL,
+                         "note": "RLMP limiter is FP64-bound; see fp64 + step keys"},
+            "step_roofline": {"achieved": step_gbs, "peak": hbm, "unit": "GB/s",
+                              "frac": step_gbs / hbm, "bytes_per_update": BYTES_PER_UPDATE},
+            "kernel_ms_per_step": {"k_theta": theta_ms, "k_advance": adv_ms, "k_sched": sched_ms},
+            "clocks": clk.summary(),
+        }
+        if e2e:
+            line["e2e"] = e2e
+        if post:
+            line["postproc"] = post
+        if not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_reference(args, ws)
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -209,6 +209,22 @@ int vlbm_ensemble_moments(int M, int64_t n_cells, const double* samples, double*
  * sequential summation order (bit-exact). */
 int vlbm_d_strong_partials(int M, int nxc, int nyc, const double* d_coarse, const double* d_fine,
                            double* d_partials, void* stream);
+/* One variable (e.g. rho planes only, BASELINE configs[3]): coarse(m, c) =
+ * d_coarse[m*c_stride + c]; the fine plane of sample m (2nxc x 2nyc) starts
+ * at d_fine + m*f_stride and is restricted on the fly.  Writes M x 10
+ * partials like vlbm_d_strong_partials (components 1..3 zero): equal to the
+ * 4-component sums when the other components are identically zero. */
+int vlbm_d_strong_partials_var(int M, int nxc, int nyc, const double* d_coarse, int64_t c_stride,
+                               const double* d_fine, int64_t f_stride, double* d_partials,
+                               void* stream);
+/* strong_error's host tail (metrics.hpp:81-89) over M x 10 partials (host
+ * copy): throws-equivalent VLBM_E_DOMAIN on a zero reference norm. */
+int vlbm_strong_finish(int M, const double* partials, double* result, double* per_component);
+/* W1 per-cell terms of coarse planes vs the on-the-fly restriction of fine
+ * planes (one variable, addressing as vlbm_d_strong_partials_var). */
+int vlbm_d_w1_restrict(int M, int nxc, int nyc, const double* d_coarse, int64_t c_stride,
+                       const double* d_fine, int64_t f_stride, double* d_cell_terms,
+                       void* stream);
 /* Restricted-fine plane of one variable into a (M x n_cells) array. */
 int vlbm_d_restrict_var(int M, int nxc, int nyc, const double* d_fine, int var, double* d_out,
                         void* stream);

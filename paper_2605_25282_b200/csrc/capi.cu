@@ -596,6 +596,30 @@ int vlbm_d_strong_partials(int M, int nxc, int nyc, const double* d_coarse, cons
   return VLBM_OK;
 }
 
+int vlbm_d_strong_partials_var(int M, int nxc, int nyc, const double* d_coarse, int64_t c_stride,
+                               const double* d_fine, int64_t f_stride, double* d_partials,
+                               void* stream) {
+  if (M < 1) return set_error(VLBM_E_INVALID, "strong_error: sample counts differ or are empty");
+  CU(vlbm_impl::launch_strong_partials_var(M, nxc, nyc, d_coarse, c_stride, d_fine, f_stride,
+                                           d_partials, (cudaStream_t)stream));
+  return VLBM_OK;
+}
+
+int vlbm_strong_finish(int M, const double* partials, double* result, double* per_component) {
+  if (M < 1 || !partials || !result)
+    return set_error(VLBM_E_INVALID, "strong_error: sample counts differ or are empty");
+  std::vector<double> part(partials, partials + 10 * (size_t)M);
+  return strong_finish(M, part, result, per_component);
+}
+
+int vlbm_d_w1_restrict(int M, int nxc, int nyc, const double* d_coarse, int64_t c_stride,
+                       const double* d_fine, int64_t f_stride, double* d_terms, void* stream) {
+  if (M < 1 || M > 1024) return set_error(VLBM_E_INVALID, "wasserstein1: 1 <= M <= 1024");
+  CU(vlbm_impl::launch_w1_restrict(M, nxc, nyc, d_coarse, c_stride, d_fine, f_stride, d_terms,
+                                   (cudaStream_t)stream));
+  return VLBM_OK;
+}
+
 int vlbm_d_restrict_var(int M, int nxc, int nyc, const double* d_fine, int var, double* d_out,
                         void* stream) {
   CU(vlbm_impl::launch_restrict_var(M, nxc, nyc, d_fine, var, d_out, (cudaStream_t)stream));

@@ -48,6 +48,11 @@ cudaError_t launch_restrict_var(int M, int nxc, int nyc, const double* fine, int
 // per-sample sequential L1 partials (num, den, cnum[4], cden[4]) -> M x 10
 cudaError_t launch_strong_partials(int M, int64_t n, const double* a, const double* b,
                                    double* partials, cudaStream_t st);
+// one variable, fused restriction: coarse(m, c) = coarse[m*c_stride + c],
+// fine plane of sample m at fine + m*f_stride
+cudaError_t launch_strong_partials_var(int M, int nxc, int nyc, const double* coarse,
+                                       int64_t c_stride, const double* fine, int64_t f_stride,
+                                       double* partials, cudaStream_t st);
 cudaError_t launch_strong_partials_fused(int M, int nxc, int nyc, const double* coarse,
                                          const double* fine, double* partials, cudaStream_t st);
 cudaError_t launch_w1_planes(int M, int64_t n, const double* a, int64_t a_sample_stride,

@@ -66,30 +66,37 @@ __global__ void k_restrict_var(int M, int nxc, int nyc, const double* fine, int 
 // order, exactly as metrics.hpp:71-80.
 constexpr int kSpChunk = 256;  // cells per chunk
 
-template <bool kFused>
+// Addressing: a(m, k, c) = a[m*as + k*ac + c]; b likewise with (bs, bc), or
+// with kFused the restriction of the fine plane at b + m*bs + k*bc.  kNC = 1
+// sums one variable only: when the other components are identically zero
+// (BASELINE configs[3]) the reference's 4-component sums add only +0.0 terms,
+// so the result is bit-identical.
+template <bool kFused, int kNC>
 __global__ void __launch_bounds__(128) k_strong_partials(int M, long long n, int nxc,
-                                                         const double* a, const double* b,
+                                                         const double* a, long long as,
+                                                         long long ac, const double* b,
+                                                         long long bs, long long bc,
                                                          double* partials) {
-  __shared__ double sd[2][kSpChunk * 4];
-  __shared__ double sr[2][kSpChunk * 4];
+  __shared__ double sd[2][kSpChunk * kNC];
+  __shared__ double sr[2][kSpChunk * kNC];
   const int m = blockIdx.x;
-  const double* A = a + (long long)m * 4 * n;
-  const double* B = b + (long long)m * 4 * n * (kFused ? 4 : 1);
+  const double* A = a + (long long)m * as;
+  const double* B = b + (long long)m * bs;
   const long long nchunks = (n + kSpChunk - 1) / kSpChunk;
   auto stage = [&](long long ch, int buf, int t0, int nt) {
     const long long c0 = ch * kSpChunk;
-    for (int q = t0; q < kSpChunk * 4; q += nt) {
-      const int cl = q >> 2, k = q & 3;
+    for (int q = t0; q < kSpChunk * kNC; q += nt) {
+      const int cl = q / kNC, k = q % kNC;
       const long long c = c0 + cl;
       if (c < n) {
         double bv;
         if (kFused) {
           const int j = (int)(c / nxc), i = (int)(c - (long long)j * nxc);
-          bv = restrict_at(B + (long long)k * 4 * n, 2 * nxc, i, j);
+          bv = restrict_at(B + (long long)k * bc, 2 * nxc, i, j);
         } else {
-          bv = B[(long long)k * n + c];
+          bv = B[(long long)k * bc + c];
         }
-        const double av = A[(long long)k * n + c];
+        const double av = A[(long long)k * ac + c];
         sd[buf][q] = fabs(av - bv);
         sr[buf][q] = fabs(bv);
       }
@@ -108,8 +115,8 @@ __global__ void __launch_bounds__(128) k_strong_partials(int M, long long n, int
       const int nc = (int)((n - c0) < kSpChunk ? (n - c0) : kSpChunk);
       for (int cl = 0; cl < nc; ++cl) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const double d = sd[buf][cl * 4 + k], r = sr[buf][cl * 4 + k];
+        for (int k = 0; k < kNC; ++k) {
+          const double d = sd[buf][cl * kNC + k], r = sr[buf][cl * kNC + k];
           num += d;
           den += r;
           cnum[k] += d;
@@ -321,19 +328,26 @@ cudaError_t launch_restrict_var(int M, int nxc, int nyc, const double* fine, int
 
 cudaError_t launch_strong_partials(int M, int64_t n, const double* a, const double* b,
                                    double* partials, cudaStream_t st) {
-  k_strong_partials<false><<<M, 128, 0, st>>>(M, n, 0, a, b, partials);
+  k_strong_partials<false, 4><<<M, 128, 0, st>>>(M, n, 0, a, 4 * n, n, b, 4 * n, n, partials);
   return cudaGetLastError();
 }
 
 cudaError_t launch_strong_partials_fused(int M, int nxc, int nyc, const double* coarse,
                                          const double* fine, double* partials, cudaStream_t st) {
-  k_strong_partials<true><<<M, 128, 0, st>>>(M, (long long)nxc * nyc, nxc, coarse, fine,
-                                             partials);
+  const long long n = (long long)nxc * nyc;
+  k_strong_partials<true, 4><<<M, 128, 0, st>>>(M, n, nxc, coarse, 4 * n, n, fine, 16 * n, 4 * n,
+                                                partials);
   return cudaGetLastError();
 }
 
-template <template <int> class K>
-struct Dispatch;
+cudaError_t launch_strong_partials_var(int M, int nxc, int nyc, const double* coarse,
+                                       int64_t c_stride, const double* fine, int64_t f_stride,
+                                       double* partials, cudaStream_t st) {
+  const long long n = (long long)nxc * nyc;
+  k_strong_partials<true, 1><<<M, 128, 0, st>>>(M, n, nxc, coarse, c_stride, 0, fine, f_stride,
+                                                0, partials);
+  return cudaGetLastError();
+}
 
 #define W1_DISPATCH(KERNEL, M, grid, st, ...)                                   \
   do {                                                                          \

@@ -1,0 +1,83 @@
+"""Device-resident W1/L1 post-processing on torch CUDA tensors (torch is only
+the allocator/stream plumbing; every number comes from post.cu via the C ABI).
+
+The ensemble layout is sample-major planes of one variable: ``coarse`` is
+(M, nyc, nxc), ``fine`` is (M, 2*nyc, 2*nxc), both float64 on one device.
+The restriction of the fine ensemble (restrict_field, metrics.hpp:29-49) is
+fused into both reductions.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from .vlbm import _check, lib
+
+
+def _ptr(t) -> int:
+    return t.data_ptr()
+
+
+def _stream(torch, t) -> int:
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def _check_pair(coarse, fine):
+    if coarse.dtype != fine.dtype or str(coarse.dtype) != "torch.float64":
+        raise ValueError("expected float64 tensors")
+    M, nyc, nxc = coarse.shape
+    if fine.shape != (M, 2 * nyc, 2 * nxc):
+        raise ValueError("wasserstein1: inconsistent field sizes")
+    if not (coarse.is_contiguous() and fine.is_contiguous()):
+        raise ValueError("expected contiguous tensors")
+    return M, nyc, nxc
+
+
+def w1_cell_terms(torch, coarse, fine, out=None):
+    """Per-cell W1 terms sum_m |a_(m) - b_(m)| / M (metrics.hpp:113-122)."""
+    M, nyc, nxc = _check_pair(coarse, fine)
+    if out is None:
+        out = torch.empty(nyc * nxc, dtype=torch.float64, device=coarse.device)
+    _check(lib().vlbm_d_w1_restrict(M, nxc, nyc, _ptr(coarse), nyc * nxc, _ptr(fine),
+                                    4 * nyc * nxc, _ptr(out), _stream(torch, coarse)))
+    return out
+
+
+def ordered_mean(torch, terms, out=None):
+    """Storage-order sequential mean of the per-cell terms (bit-exact acc)."""
+    if out is None:
+        out = torch.empty(1, dtype=torch.float64, device=terms.device)
+    _check(lib().vlbm_d_ordered_mean(terms.numel(), _ptr(terms), _ptr(out),
+                                     _stream(torch, terms)))
+    return out
+
+
+def wasserstein1(torch, coarse, fine) -> float:
+    """wasserstein1(coarse, restrict(fine)) over one variable (bit-exact)."""
+    return float(ordered_mean(torch, w1_cell_terms(torch, coarse, fine)).item())
+
+
+def strong_partials(torch, coarse, fine, out=None):
+    """Per-sample (num, den, cnum[4], cden[4]) of strong_error in the
+    reference's sequential order, one variable, restriction fused."""
+    M, nyc, nxc = _check_pair(coarse, fine)
+    if out is None:
+        out = torch.empty((M, 10), dtype=torch.float64, device=coarse.device)
+    _check(lib().vlbm_d_strong_partials_var(M, nxc, nyc, _ptr(coarse), nyc * nxc, _ptr(fine),
+                                            4 * nyc * nxc, _ptr(out), _stream(torch, coarse)))
+    return out
+
+
+def strong_finish(partials) -> float:
+    p = np.ascontiguousarray(partials, np.float64)
+    r = C.c_double()
+    pc = np.zeros(4)
+    _check(lib().vlbm_strong_finish(p.shape[0], p.ctypes.data_as(C.POINTER(C.c_double)),
+                                    C.byref(r), pc.ctypes.data_as(C.POINTER(C.c_double))))
+    return r.value
+
+
+def strong_error(torch, coarse, fine) -> float:
+    """strong_error(coarse, restrict(fine)) when only this variable is nonzero."""
+    return strong_finish(strong_partials(torch, coarse, fine).cpu().numpy())

@@ -187,6 +187,9 @@ def lib() -> C.CDLL:
     sig("vlbm_wasserstein1", I, [I, I64, DP, DP, I, DP])
     sig("vlbm_ensemble_moments", I, [I, I64, DP, DP, DP])
     sig("vlbm_d_strong_partials", I, [I, I, I, V, V, V, V])
+    sig("vlbm_d_strong_partials_var", I, [I, I, I, V, I64, V, I64, V, V])
+    sig("vlbm_strong_finish", I, [I, DP, DP, DP])
+    sig("vlbm_d_w1_restrict", I, [I, I, I, V, I64, V, I64, V, V])
     sig("vlbm_d_restrict_var", I, [I, I, I, V, I, V, V])
     sig("vlbm_d_w1_cells", I, [I, I64, V, V, V, V])
     sig("vlbm_d_w1_cells_planes", I, [I, I64, V, V, V, V])

@@ -1,0 +1,163 @@
+"""GPU parity of the W1/L1 post-processing (-m gpu), against the reference
+itself (oracle/_ref) where it is present, else the pinned C restatement.
+
+W1, restriction and moments must be BIT-EXACT (north_star: "W1 must be
+bit-exact given identical input fields"); strong_error is bit-exact too
+(the device keeps the reference's sequential summation order)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def oc():
+    from oracle import oracle
+    return oracle.Oracle("ref" if oracle.available("ref") else "vo")
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float64).view(np.uint64)
+
+
+def ens(rng, M, ny, nx, ties=False):
+    x = rng.lognormal(-0.125, 0.5, size=(M, 4, ny, nx))
+    x[:, 1:3] = rng.normal(size=(M, 2, ny, nx))
+    if ties:
+        x = np.round(x * 4) / 4  # many equal values
+        x[:, 2, 0, 0] = -0.0
+        x[:M // 2, 2, 0, 1] = 0.0
+        x[M // 2:, 2, 0, 1] = -0.0
+    return x
+
+
+def test_restrict_field_bitwise(vlbm, oc):
+    rng = np.random.default_rng(1)
+    f = rng.normal(size=(4, 10, 14))
+    assert np.array_equal(bits(vlbm.restrict_field(f)), bits(oc.restrict_field(f)))
+    # KAT: a 2x2 block {1,2,3,6} -> 3 (test_metrics.cpp:43-49)
+    blk = np.zeros((4, 2, 2))
+    blk[0] = [[1.0, 2.0], [3.0, 6.0]]
+    assert vlbm.restrict_field(blk)[0, 0, 0] == 3.0
+    with pytest.raises(ValueError):
+        vlbm.restrict_field(np.zeros((4, 5, 5)))
+
+
+@pytest.mark.parametrize("M", [1, 2, 3, 8, 33])
+def test_strong_error_bitwise(vlbm, oc, M):
+    rng = np.random.default_rng(M)
+    a, b = ens(rng, M, 6, 9), ens(rng, M, 6, 9)
+    got, gpc = vlbm.strong_error(a, b, per_component=True)
+    want, wpc = oc.strong_error(a, b)
+    assert bits(got) == bits(want)
+    assert np.array_equal(bits(gpc), bits(wpc))
+
+
+def test_strong_error_kats(vlbm):
+    """test_metrics.cpp:77-103."""
+    a = np.zeros((1, 4, 4, 4))
+    b = np.zeros((1, 4, 4, 4))
+    a[:, 0], b[:, 0] = 4.0, 3.0
+    assert abs(vlbm.strong_error(a, b) - 1.0 / 3.0) <= 1e-14
+    c = np.broadcast_to(np.array([1.0, 2.0, -1.0, 5.0])[None, :, None, None], (1, 4, 4, 4))
+    assert vlbm.strong_error(c, c) == 0.0
+    with pytest.raises(ArithmeticError):
+        vlbm.strong_error(a, np.zeros_like(b))
+    with pytest.raises(ValueError):
+        vlbm.strong_error(a, np.zeros((0, 4, 4, 4)))
+
+
+@pytest.mark.parametrize("M", [1, 2, 5, 31, 32, 33, 64, 100, 257, 1000])
+@pytest.mark.parametrize("ties", [False, True])
+def test_wasserstein1_bitwise(vlbm, oc, M, ties):
+    rng = np.random.default_rng(M + 7 * ties)
+    ny, nx = (3, 5) if M >= 257 else (6, 7)
+    a, b = ens(rng, M, ny, nx, ties), ens(rng, M, ny, nx, ties)
+    for var in (0, 2):
+        got = vlbm.wasserstein1(a, b, var)
+        want = oc.wasserstein1(a, b, var)
+        assert bits(got) == bits(want), (M, var, got, want)
+
+
+def test_wasserstein1_kats_and_ot(vlbm, ref):
+    """test_metrics.cpp:106-122: hand values and the brute-force OT oracle."""
+    def w1s(x, y):
+        A = np.zeros((len(x), 4, 4, 4))
+        B = np.zeros((len(y), 4, 4, 4))
+        A[:, 0] = np.asarray(x)[:, None, None]
+        B[:, 0] = np.asarray(y)[:, None, None]
+        return vlbm.wasserstein1(A, B, 0)
+
+    assert w1s([0.0, 1.0], [1.0, 0.0]) == 0.0
+    assert w1s([0.0, 0.0], [1.0, 3.0]) == 2.0
+    assert w1s([1.0], [4.0]) == 3.0
+    rng = np.random.default_rng(321)
+    for _ in range(100):
+        m = int(rng.integers(2, 9))
+        x, y = 10 * rng.uniform(-1, 1, m), 10 * rng.uniform(-1, 1, m)
+        o = ref.ot_oracle(x, y)
+        assert abs(w1s(x, y) - o) <= 1e-12 * (1 + abs(o))
+
+def test_wasserstein1_equals_assignment_oracle_criterion4(vlbm, ref):
+    """acceptance.cpp:196-234 (criterion 4) verbatim in intent: 500 trials of
+    dyadic-lattice values on a 1x1 grid from SplitMix64(321); W1 must equal
+    the brute-force assignment minimum bit-for-bit."""
+    state = [321]
+    mask = (1 << 64) - 1
+
+    def next_u64():
+        state[0] = (state[0] + 0x9E3779B97F4A7C15) & mask
+        z = state[0]
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & mask
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & mask
+        return z ^ (z >> 31)
+
+    def draw():
+        return (float(next_u64() % 20481) - 10240.0) / 1024.0
+
+    bad = 0
+    for _ in range(500):
+        m = 2 + next_u64() % 7
+        a = [draw() for _ in range(m)]
+        b = [draw() for _ in range(m)]
+        A = np.zeros((m, 4, 1, 1))
+        B = np.zeros((m, 4, 1, 1))
+        A[:, 0, 0, 0] = a
+        B[:, 0, 0, 0] = b
+        if vlbm.wasserstein1(A, B, 0) != ref.ot_oracle(np.array(a), np.array(b)):
+            bad += 1
+    assert bad == 0
+
+
+@pytest.mark.parametrize("M", [2, 3, 64])
+def test_moments_bitwise(vlbm, oc, M):
+    rng = np.random.default_rng(M)
+    x = ens(rng, M, 5, 6)
+    gm, gs = vlbm.ensemble_moments(x)
+    wm, ws = oc.ensemble_moments(x)
+    assert np.array_equal(bits(gm), bits(wm)) and np.array_equal(bits(gs), bits(ws))
+    with pytest.raises(ValueError):
+        vlbm.ensemble_moments(x[:1])
+
+
+@pytest.mark.parametrize("M,nxc,nyc", [(5, 6, 4), (64, 20, 6), (1000, 8, 4)])
+def test_device_pipeline_c4_style(vlbm, oc, M, nxc, nyc):
+    """Density-plane pipeline (fused restriction) == reference
+    wasserstein1(coarse, restrict_field(fine)) and strong_error with the
+    other components zero, bit-for-bit."""
+    import torch
+    from paper_2605_25282_b200 import post
+    rng = np.random.default_rng(M)
+    c = rng.lognormal(-0.125, 0.5, size=(M, nyc, nxc))
+    f = rng.lognormal(-0.125, 0.5, size=(M, 2 * nyc, 2 * nxc))
+    tc = torch.from_numpy(c).cuda()
+    tf = torch.from_numpy(f).cuda()
+    w1 = post.wasserstein1(torch, tc, tf)
+    es = post.strong_error(torch, tc, tf)
+    C4 = np.zeros((M, 4, nyc, nxc))
+    C4[:, 0] = c
+    F4 = np.zeros((M, 4, 2 * nyc, 2 * nxc))
+    F4[:, 0] = f
+    R4 = np.stack([oc.restrict_field(F4[m]) for m in range(M)])
+    assert bits(w1) == bits(oc.wasserstein1(C4, R4, 0))
+    assert bits(es) == bits(oc.strong_error(C4, R4)[0])
