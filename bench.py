@@ -230,6 +230,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--samples", type=int, default=M_PER_GPU)
+    ap.add_argument("--t-start", type=float, default=0.0,
+                    help="march every sample to this time (untimed) before the warmup")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-postproc", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -260,6 +262,8 @@ def main():
     sim = v.BatchSimulation.jet(g, lat, gas, pp, base_seed=42, m0=rank * M, n_samples=M,
                                 device=local)
     stream = torch.cuda.ExternalStream(sim.stream(), device=torch.device("cuda", local))
+    if args.t_start > 0:
+        sim.run_to(args.t_start)
     sim.step(args.warmup)
     sim.set_timing(True)
     st0 = sim.stats()

@@ -84,6 +84,9 @@ void free_batch(vlbm_batch* b) {
   cudaFree(b->P.ctl);
   cudaFree(b->P.n_active);
   cudaFree(b->d_a0);
+  cudaFree(b->P.hq);
+  cudaFree(b->P.hq_idx);
+  cudaFree(b->P.hq_n);
   cudaFree(b->d_face_tx);
   cudaFree(b->d_face_ty);
   if (b->h_active) cudaFreeHost(b->h_active);
@@ -151,6 +154,22 @@ int alloc_batch(const vlbm_grid* g, const vlbm_params* p, int S, int device, vlb
   chk(cudaMalloc(&P.n_active, sizeof(int)), "malloc n_active");
   chk(cudaMalloc(&b->d_a0, sizeof(double) * S), "malloc a0");
   chk(cudaMallocHost(&b->h_active, sizeof(int)), "malloc host");
+  // Limiter hard-cell queue: up to every cell of the batch, capped by memory
+  // (overflowing CTAs finish their hard cells in place).
+  if (p->limiter == VLBM_LIMITER_RLMP && rc == VLBM_OK) {
+    const size_t entry = sizeof(double) * vlbm_dev::kHardWords + sizeof(long long);
+    size_t cap = (size_t)S * P.nx * P.ny;
+    size_t avail = free_b > need + (size_t)(2ull << 30) ? free_b - need - (size_t)(2ull << 30) : 0;
+    if (cap * entry > avail / 2) cap = avail / 2 / entry;
+    if (cap > (size_t)INT_MAX / 2) cap = (size_t)INT_MAX / 2;
+    if (cap >= 1024) {
+      P.hq_cap = (int)cap;
+      chk(cudaMalloc(&P.hq, sizeof(double) * vlbm_dev::kHardWords * cap), "malloc hq");
+      chk(cudaMalloc(&P.hq_idx, sizeof(long long) * cap), "malloc hq_idx");
+      chk(cudaMalloc(&P.hq_n, sizeof(int)), "malloc hq_n");
+      if (rc == VLBM_OK) chk(cudaMemset(P.hq_n, 0, sizeof(int)), "memset hq_n");
+    }
+  }
   if (rc == VLBM_OK) {
     chk(cudaMemsetAsync(P.buf0, 0, state_bytes, b->stream), "memset");
     chk(cudaMemsetAsync(P.buf1, 0, state_bytes, b->stream), "memset");
@@ -248,7 +267,7 @@ int march_loop(vlbm_batch* b, double target, double fixed_dt, int mode, int chun
       record(b, 2);
       CU(vlbm_impl::launch_advance(P, adv_mode, const_theta, b->stream));
       record_end(b);
-      b->launches += rlmp ? 3 : 2;
+      b->launches += rlmp ? (P.hq ? 4 : 3) : 2;
     }
     CU(cudaMemcpyAsync(b->h_active, P.n_active, sizeof(int), cudaMemcpyDeviceToHost, b->stream));
     CU(cudaStreamSynchronize(b->stream));

@@ -263,7 +263,10 @@ __global__ void k_sched(MarchParams P, double target, double fixed_dt) {
   __syncthreads();
   if (count) atomicAdd(&s_count, count);
   __syncthreads();
-  if (threadIdx.x == 0) *P.n_active = s_count;
+  if (threadIdx.x == 0) {
+    *P.n_active = s_count;
+    if (P.hq_n) *P.hq_n = 0;  // empty hard-cell queue for the coming limiter pass
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -690,9 +693,26 @@ __global__ void __launch_bounds__(tiled::NT, 2) k_theta_tiled(MarchParams P, int
   }
   __syncthreads();
 
-  // Phase 4: the cells that failed theta = 1, compacted onto the first warps
-  // so the 30-step bisections do not serialise whole warps of easy cells.
+  // Phase 4: the cells that failed theta = 1 go to the global hard-cell queue
+  // (one atomic per CTA), processed by k_theta_hard at full occupancy so the
+  // 30-step bisections neither serialise warps of easy cells nor keep this
+  // CTA resident.  If the queue is full they are finished here instead.
   const int n = qn;
+  if (n == 0) return;
+  __shared__ int qbase;
+  if (threadIdx.x == 0) qbase = P.hq ? atomicAdd(P.hq_n, n) : P.hq_cap;
+  __syncthreads();
+  const int base = qbase;
+  if (base + n <= P.hq_cap) {
+    for (int slot = threadIdx.x; slot < n; slot += NT) {
+#pragma unroll 4
+      for (int k = 0; k < kHardWords; ++k)
+        P.hq[(long long)k * P.hq_cap + base + slot] = Q[k * NT + slot];
+      P.hq_idx[base + slot] = (long long)s * P.plane + qidx[slot];
+    }
+    return;
+  }
+  for (int slot = base + threadIdx.x; slot < P.hq_cap; slot += NT) P.hq_idx[slot] = -1;
   for (int slot = threadIdx.x; slot < n; slot += NT) {
     const cs fo = {Q[0 * NT + slot], Q[1 * NT + slot], Q[2 * NT + slot], Q[3 * NT + slot]};
     cs cf[4];
@@ -709,6 +729,33 @@ __global__ void __launch_bounds__(tiled::NT, 2) k_theta_tiled(MarchParams P, int
     b.p_floor = P.p_floor_coef;
     const double th = rlmp_theta_hard(fo, cf, b, gm1);
     P.theta[(long long)s * P.plane + qidx[slot]] = th;
+  }
+}
+
+// The limiter's hard cells from the global queue (rlmp_theta after a failed
+// feasible(1.0), solver.hpp:462-486), one thread per cell, grid-stride.
+__global__ void __launch_bounds__(256, 2) k_theta_hard(MarchParams P) {
+  const int n = min(*P.hq_n, P.hq_cap);
+  const long long cap = P.hq_cap;
+  for (int slot = blockIdx.x * blockDim.x + threadIdx.x; slot < n;
+       slot += gridDim.x * blockDim.x) {
+    const long long idx = P.hq_idx[slot];
+    if (idx < 0) continue;
+    const double* q = P.hq + slot;
+    const cs fo = {q[0], q[cap], q[2 * cap], q[3 * cap]};
+    cs cf[4];
+#pragma unroll
+    for (int f = 0; f < 4; ++f)
+      cf[f] = {q[(4 + 4 * f) * cap], q[(5 + 4 * f) * cap], q[(6 + 4 * f) * cap],
+               q[(7 + 4 * f) * cap]};
+    RlmpBounds b;
+    b.rho_lo = q[20 * cap];
+    b.rho_hi = q[21 * cap];
+    b.p_lo = q[22 * cap];
+    b.p_hi = q[23 * cap];
+    b.rho_floor = P.rho_floor_coef;
+    b.p_floor = P.p_floor_coef;
+    P.theta[idx] = rlmp_theta_hard(fo, cf, b, P.gm1);
   }
 }
 
@@ -866,6 +913,7 @@ cudaError_t launch_theta(const MarchParams& P, cudaStream_t st) {
   int tx;
   const dim3 g = tiled_grid(P, tx);
   k_theta_tiled<<<g, tiled::NT, tiled::kThetaSmem, st>>>(P, tx);
+  if (P.hq) k_theta_hard<<<148 * 8, 256, 0, st>>>(P);
   return cudaGetLastError();
 }
 

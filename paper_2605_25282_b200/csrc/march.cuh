@@ -20,6 +20,7 @@ enum { BC_INLET = 0, BC_OUTFLOW = 1, BC_WALL = 2, BC_PERIODIC = 3 };
 enum { LIM_FIRST = 0, LIM_SECOND = 1, LIM_RLMP = 2 };
 enum { ST_RUNNING = 0, ST_DIVERGED = 2 };
 constexpr int kPlanes = 20;
+constexpr int kHardWords = 24;  // u_FO (4), c_w/c_e/c_s/c_n (16), rho_lo/hi, p_lo/hi
 
 // Per-sample control block.  Written by k_sched (one thread per sample) and
 // by the advance epilogue (atomics on smax_bits / flags).
@@ -51,6 +52,12 @@ struct MarchParams {
   const double* face_ty;    // (S x (ny+1) x nx)
   SampleCtl* ctl;
   int* n_active;
+  // Global hard-cell queue of the limiter (cells that fail theta = 1): SoA,
+  // kHardWords doubles per entry, capacity hq_cap; hq_n is reset by k_sched.
+  double* hq;
+  long long* hq_idx;  // s * plane + j * pitch + i
+  int* hq_n;
+  int hq_cap;
   double dx, gamma, gm1, alpha, w, safety, kappa, rho_floor_coef, p_floor_coef;
   double rho_ref, p_ref;
   int bc[4];
