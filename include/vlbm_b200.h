@@ -187,6 +187,13 @@ void* vlbm_batch_stream(vlbm_batch* b);
 int vlbm_batch_set_timing(vlbm_batch* b, int enable);
 int vlbm_batch_stats(vlbm_batch* b, int64_t* launches, double* ms_theta, double* ms_advance,
                      double* ms_sched, int64_t* cell_updates);
+/* Audit of the limiter's certified bisection (test hook): when enabled, every
+ * certified bisection step also runs the full 16-check feasible() and counts
+ * disagreements.  vlbm_batch_audit fills counters[4]: disagreements (must be
+ * 0), bisections entered, bisections certified, vertex-floor failures at the
+ * closed-form theta. */
+int vlbm_batch_set_audit(vlbm_batch* b, int enable);
+int vlbm_batch_audit(vlbm_batch* b, int64_t* counters);
 
 /* ---- post-processing (host buffers, synchronous) ---------------------- */
 /* restrict_field: fine nx x ny (even) field block -> (nx/2) x (ny/2). */

@@ -87,8 +87,13 @@ void free_batch(vlbm_batch* b) {
   cudaFree(b->P.hq);
   cudaFree(b->P.hq_idx);
   cudaFree(b->P.hq_n);
+  cudaFree(b->P.bq);
+  cudaFree(b->P.bq_idx);
+  cudaFree(b->P.cq);
+  cudaFree(b->P.cq_idx);
   cudaFree(b->d_face_tx);
   cudaFree(b->d_face_ty);
+  cudaFree(b->P.audit);
   if (b->h_active) cudaFreeHost(b->h_active);
   for (cudaEvent_t e : b->ev) cudaEventDestroy(e);
   if (b->stream) cudaStreamDestroy(b->stream);
@@ -157,7 +162,9 @@ int alloc_batch(const vlbm_grid* g, const vlbm_params* p, int S, int device, vlb
   // Limiter hard-cell queue: up to every cell of the batch, capped by memory
   // (overflowing CTAs finish their hard cells in place).
   if (p->limiter == VLBM_LIMITER_RLMP && rc == VLBM_OK) {
-    const size_t entry = sizeof(double) * vlbm_dev::kHardWords + sizeof(long long);
+    const size_t entry =
+        sizeof(double) * (vlbm_dev::kHardWords + vlbm_dev::kBisWords + vlbm_dev::kUncWords) +
+        3 * sizeof(long long);
     size_t cap = (size_t)S * P.nx * P.ny;
     size_t avail = free_b > need + (size_t)(2ull << 30) ? free_b - need - (size_t)(2ull << 30) : 0;
     if (cap * entry > avail / 2) cap = avail / 2 / entry;
@@ -166,8 +173,13 @@ int alloc_batch(const vlbm_grid* g, const vlbm_params* p, int S, int device, vlb
       P.hq_cap = (int)cap;
       chk(cudaMalloc(&P.hq, sizeof(double) * vlbm_dev::kHardWords * cap), "malloc hq");
       chk(cudaMalloc(&P.hq_idx, sizeof(long long) * cap), "malloc hq_idx");
-      chk(cudaMalloc(&P.hq_n, sizeof(int)), "malloc hq_n");
-      if (rc == VLBM_OK) chk(cudaMemset(P.hq_n, 0, sizeof(int)), "memset hq_n");
+      chk(cudaMalloc(&P.bq, sizeof(double) * vlbm_dev::kBisWords * cap), "malloc bq");
+      chk(cudaMalloc(&P.bq_idx, sizeof(long long) * cap), "malloc bq_idx");
+      chk(cudaMalloc(&P.cq, sizeof(double) * vlbm_dev::kUncWords * cap), "malloc cq");
+      chk(cudaMalloc(&P.cq_idx, sizeof(long long) * cap), "malloc cq_idx");
+      chk(cudaMalloc(&P.hq_n, 4 * sizeof(int)), "malloc hq_n");
+      P.hq_next = P.hq_n + 1;
+      if (rc == VLBM_OK) chk(cudaMemset(P.hq_n, 0, 4 * sizeof(int)), "memset hq_n");
     }
   }
   if (rc == VLBM_OK) {
@@ -267,7 +279,7 @@ int march_loop(vlbm_batch* b, double target, double fixed_dt, int mode, int chun
       record(b, 2);
       CU(vlbm_impl::launch_advance(P, adv_mode, const_theta, b->stream));
       record_end(b);
-      b->launches += rlmp ? (P.hq ? 4 : 3) : 2;
+      b->launches += rlmp ? (P.hq ? 6 : 3) : 2;
     }
     CU(cudaMemcpyAsync(b->h_active, P.n_active, sizeof(int), cudaMemcpyDeviceToHost, b->stream));
     CU(cudaStreamSynchronize(b->stream));
@@ -489,6 +501,30 @@ int vlbm_batch_set_timing(vlbm_batch* b, int enable) {
   if (!b) return set_error(VLBM_E_INVALID, "null batch");
   b->timing = enable != 0;
   b->ms_theta = b->ms_advance = b->ms_sched = 0;
+  return VLBM_OK;
+}
+
+int vlbm_batch_set_audit(vlbm_batch* b, int enable) {
+  if (!b) return set_error(VLBM_E_INVALID, "null batch");
+  CU(cudaSetDevice(b->device));
+  if (enable && !b->P.audit) {
+    CU(cudaMalloc(&b->P.audit, 4 * sizeof(int)));
+    CU(cudaMemset(b->P.audit, 0, 4 * sizeof(int)));
+  } else if (!enable && b->P.audit) {
+    CU(cudaFree(b->P.audit));
+    b->P.audit = nullptr;
+  }
+  return VLBM_OK;
+}
+
+int vlbm_batch_audit(vlbm_batch* b, int64_t* counters) {
+  if (!b || !counters) return set_error(VLBM_E_INVALID, "null argument");
+  int h[4] = {0, 0, 0, 0};
+  if (b->P.audit) {
+    CU(cudaMemcpyAsync(h, b->P.audit, sizeof(h), cudaMemcpyDeviceToHost, b->stream));
+    CU(cudaStreamSynchronize(b->stream));
+  }
+  for (int k = 0; k < 4; ++k) counters[k] = h[k];
   return VLBM_OK;
 }
 

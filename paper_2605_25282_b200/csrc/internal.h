@@ -37,6 +37,10 @@ cudaError_t launch_theta(const vlbm_dev::MarchParams& P, cudaStream_t st);
 // mode 0: cell theta plane, 1: constant theta, 2: prescribed faces
 cudaError_t launch_advance(const vlbm_dev::MarchParams& P, int mode, double const_theta,
                            cudaStream_t st);
+// tiled production kernels (march_tiled.cu)
+cudaError_t launch_theta_tiled(const vlbm_dev::MarchParams& P, cudaStream_t st);
+cudaError_t launch_advance_tiled(const vlbm_dev::MarchParams& P, int mode, double const_theta,
+                                 cudaStream_t st);
 cudaError_t launch_set_budget(const vlbm_dev::MarchParams& P, long long budget,
                               cudaStream_t st);
 

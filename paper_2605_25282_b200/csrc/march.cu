@@ -15,132 +15,13 @@
 // (vlbm_device.cuh); build with --fmad=false.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "march.cuh"
+#include "march_common.cuh"
 #include "rlmp.cuh"
 
 namespace vlbm_dev {
-
-// ---------------------------------------------------------------------------
-// Boundary-ring synthesis.  A padded coordinate (i, j), -2 <= i < nx+2,
-// -2 <= j < ny+2, resolves to the interior cell whose value the reference's
-// fill_ghosts copies into it: y sides first map the row (wall mirror or
-// periodic wrap, solver.hpp:270-285), then x sides map the column at that row
-// (inlet / outflow copy / periodic wrap, solver.hpp:234-269).  Corners
-// therefore see the x-side value of the mirrored row, exactly as the
-// reference fills them (x sides first, then y across the full width).
-struct Src {
-  int i, j;
-  bool mirror;  // wall: mom_y negated, pops 2 <-> 3 (set_wall_ghost :218-228)
-  bool inlet;   // inlet ghost: u = u_in(row j), pops = M_k(u_in, a) (:236-243)
-};
-
-__device__ __forceinline__ Src resolve(const MarchParams& P, int i, int j) {
-  Src r{i, j, false, false};
-  if (j < 0) {
-    if (P.bc[2] == BC_WALL) {
-      r.j = -1 - j;
-      r.mirror = true;
-    } else {
-      r.j = j + P.ny;
-    }
-  } else if (j >= P.ny) {
-    if (P.bc[3] == BC_WALL) {
-      r.j = 2 * P.ny - 1 - j;
-      r.mirror = true;
-    } else {
-      r.j = j - P.ny;
-    }
-  }
-  if (i < 0) {
-    if (P.bc[0] == BC_INLET)
-      r.inlet = true;
-    else if (P.bc[0] == BC_OUTFLOW)
-      r.i = 0;
-    else
-      r.i = i + P.nx;
-  } else if (i >= P.nx) {
-    if (P.bc[1] == BC_OUTFLOW)
-      r.i = P.nx - 1;
-    else
-      r.i = i - P.nx;
-  }
-  return r;
-}
-
-__device__ __forceinline__ cs load_plane4(const double* base, long long plane, long long off) {
-  return {base[off], base[plane + off], base[2 * plane + off], base[3 * plane + off]};
-}
-
-__device__ __forceinline__ cs inlet_row(const double* rows, int j) {
-  const double* q = rows + 4 * j;
-  return {q[0], q[1], q[2], q[3]};
-}
-
-// Macroscopic state of padded cell (i, j).
-__device__ __forceinline__ cs load_u(const MarchParams& P, const double* src, const double* rows,
-                                     int i, int j) {
-  const Src r = resolve(P, i, j);
-  cs u = r.inlet ? inlet_row(rows, r.j)
-                 : load_plane4(src, P.plane, (long long)r.j * P.pitch + r.i);
-  if (r.mirror) u.my = -u.my;
-  return u;
-}
-
-// Population k of padded cell (i, j) at kinetic speed parameter inv2a.
-__device__ __forceinline__ cs load_pop(const MarchParams& P, const double* src, const double* rows,
-                                       int k, int i, int j, double inv2a) {
-  const Src r = resolve(P, i, j);
-  const int ks = r.mirror ? (k ^ ((k >> 1) & 1)) : k;  // {0,1,3,2} under the mirror
-  cs f;
-  if (r.inlet)
-    f = maxw_k(inlet_row(rows, r.j), ks, P.w, inv2a, P.gm1);
-  else
-    f = load_plane4(src + (4 + 4 * ks) * P.plane, P.plane, (long long)r.j * P.pitch + r.i);
-  if (r.mirror) f.my = -f.my;
-  return f;
-}
-
-__device__ __forceinline__ const double* state_src(const MarchParams& P, int s, int parity) {
-  return (parity ? P.buf1 : P.buf0) + (long long)s * P.sample_stride;
-}
-__device__ __forceinline__ double* state_dst(const MarchParams& P, int s, int parity) {
-  return (parity ? P.buf0 : P.buf1) + (long long)s * P.sample_stride;
-}
-
-// ---------------------------------------------------------------------------
-// Block reduction of (max signal bits, bad, nonfinite) into the sample's ctl.
-__device__ __forceinline__ void reduce_signal(SampleCtl* c, unsigned long long bits, int bad,
-                                              int nonfin) {
-  for (int o = 16; o > 0; o >>= 1) {
-    const unsigned long long ob = __shfl_xor_sync(0xffffffffu, bits, o);
-    bits = ob > bits ? ob : bits;
-  }
-  bad = __any_sync(0xffffffffu, bad);
-  nonfin = __any_sync(0xffffffffu, nonfin);
-  __shared__ unsigned long long s_bits[32];
-  __shared__ int s_flags[32];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nw = (blockDim.x + 31) >> 5;
-  if (lane == 0) {
-    s_bits[warp] = bits;
-    s_flags[warp] = (bad ? 1 : 0) | (nonfin ? 2 : 0);
-  }
-  __syncthreads();
-  if (warp == 0) {
-    bits = lane < nw ? s_bits[lane] : 0ull;
-    int fl = lane < nw ? s_flags[lane] : 0;
-    for (int o = 16; o > 0; o >>= 1) {
-      const unsigned long long ob = __shfl_xor_sync(0xffffffffu, bits, o);
-      bits = ob > bits ? ob : bits;
-      fl |= __shfl_xor_sync(0xffffffffu, fl, o);
-    }
-    if (lane == 0) {
-      if (bits) atomicMax(&c->smax_bits, bits);
-      if (fl & 1) atomicOr(&c->bad_signal, 1);
-      if (fl & 2) atomicOr(&c->nonfinite, 1);
-    }
-  }
-}
 
 // kinetic_speed partials over the interior of the current state
 // (solver.hpp:137-145).  Used at construction.
@@ -265,7 +146,7 @@ __global__ void k_sched(MarchParams P, double target, double fixed_dt) {
   __syncthreads();
   if (threadIdx.x == 0) {
     *P.n_active = s_count;
-    if (P.hq_n) *P.hq_n = 0;  // empty hard-cell queue for the coming limiter pass
+    if (P.hq_n) P.hq_n[0] = P.hq_n[1] = P.hq_n[2] = P.hq_n[3] = 0;  // empty the limiter queues
   }
 }
 
@@ -377,64 +258,6 @@ __global__ void __launch_bounds__(256) k_theta(MarchParams P) {
   P.theta[(long long)s * P.plane + off] = th;
 }
 
-// ---------------------------------------------------------------------------
-// Face theta from cell theta (interface_theta, solver.hpp:510-534).
-__device__ __forceinline__ double cell_theta(const MarchParams& P, const double* th, int i,
-                                             int j) {
-  return th[(long long)j * P.pitch + i];
-}
-
-template <int kMode>  // 0: cell theta plane, 1: constant, 2: prescribed faces
-__device__ __forceinline__ void face_thetas(const MarchParams& P, int s, int i, int j,
-                                            double const_theta, double& tw, double& te,
-                                            double& ts, double& tn) {
-  if (kMode == 1) {
-    tw = te = ts = tn = const_theta;
-    return;
-  }
-  if (kMode == 2) {
-    const double* tx = P.face_tx + (long long)s * P.ny * (P.nx + 1);
-    const double* ty = P.face_ty + (long long)s * (P.ny + 1) * P.nx;
-    tw = tx[(long long)j * (P.nx + 1) + i];
-    te = tx[(long long)j * (P.nx + 1) + i + 1];
-    ts = ty[(long long)j * P.nx + i];
-    tn = ty[(long long)(j + 1) * P.nx + i];
-    return;
-  }
-  const double* th = P.theta + (long long)s * P.plane;
-  const int nx = P.nx, ny = P.ny;
-  const double tc = cell_theta(P, th, i, j);
-  const bool per_x = P.bc[0] == BC_PERIODIC, per_y = P.bc[2] == BC_PERIODIC;
-  if (i > 0) {
-    tw = smin(cell_theta(P, th, i - 1, j), tc);
-  } else {
-    tw = per_x ? smin(cell_theta(P, th, 0, j), cell_theta(P, th, nx - 1, j)) : tc;
-  }
-  if (i + 1 < nx) {
-    te = smin(tc, cell_theta(P, th, i + 1, j));
-  } else {
-    te = per_x ? smin(cell_theta(P, th, 0, j), cell_theta(P, th, nx - 1, j)) : tc;
-  }
-  if (j > 0) {
-    ts = smin(cell_theta(P, th, i, j - 1), tc);
-  } else {
-    ts = per_y ? smin(cell_theta(P, th, i, 0), cell_theta(P, th, i, ny - 1)) : tc;
-  }
-  if (j + 1 < ny) {
-    tn = smin(tc, cell_theta(P, th, i, j + 1));
-  } else {
-    tn = per_y ? smin(cell_theta(P, th, i, 0), cell_theta(P, th, i, ny - 1)) : tc;
-  }
-}
-
-__device__ __forceinline__ void store_plane4(double* base, long long plane, long long off,
-                                             const cs& v) {
-  base[off] = v.r;
-  base[plane + off] = v.mx;
-  base[2 * plane + off] = v.my;
-  base[3 * plane + off] = v.e;
-}
-
 // Blended stream-collide (advance, solver.hpp:536-575) + kinetic-speed and
 // state_finite epilogue for the next k_sched.
 template <int kMode>
@@ -503,330 +326,6 @@ template __global__ void k_advance<0>(MarchParams, double);
 template __global__ void k_advance<1>(MarchParams, double);
 template __global__ void k_advance<2>(MarchParams, double);
 
-// ===========================================================================
-// Tiled kernels (the production path).  A CTA owns a TX x TY tile of interior
-// cells of one sample, one thread per cell.  The macroscopic state of the tile
-// plus its halo is staged once in shared memory together with the per-cell
-// quantities every stencil neighbour needs -- u, inv2a*f(u), inv2a*g(u) and
-// p(u) -- so each flux / pressure division is evaluated once per cell instead
-// of once per use.  M_k(u) is rebuilt from the staged terms exactly as
-// maxwellians() forms it (w*u +/- inv2a*f), so every value is bit-identical to
-// the reference's.
-namespace tiled {
-constexpr int TX = 32, TY = 8, NT = TX * TY;
-// limiter: halo 2 (u at distance 2 for the allowance, M at distance 2 for u_FO)
-constexpr int RX2 = TX + 4, RY2 = TY + 4, NR2 = RX2 * RY2;
-constexpr int FX = TX + 2, FY = TY + 2, NF = FX * FY;  // u_FO ring region
-constexpr int QW = 24;                                 // doubles per hard-cell entry
-// advance: halo 1
-constexpr int RX1 = TX + 2, RY1 = TY + 2, NR1 = RX1 * RY1;
-constexpr int kStaged = 13;  // u(4), inv2a*f(4), inv2a*g(4), p
-constexpr size_t kThetaSmem = sizeof(double) * (kStaged * NR2 + 2 * NF + QW * NT) + sizeof(int) * NT;
-constexpr size_t kAdvanceSmem = sizeof(double) * (kStaged * NR1);
-}  // namespace tiled
-
-// Stage one padded cell: u, inv2a*flux_x(u), inv2a*flux_y(u), pressure(u).
-// flux_x/flux_y (euler.hpp:86-97) each evaluate pressure(u); it is computed
-// once here -- the same value.
-__device__ __forceinline__ void stage_cell(double* R, int NR, int q, const cs& u, double inv2a,
-                                           double gm1) {
-  const double p = pressure(u, gm1);
-  const double v1 = u.mx / u.r;
-  const double v2 = u.my / u.r;
-  R[q] = u.r;
-  R[NR + q] = u.mx;
-  R[2 * NR + q] = u.my;
-  R[3 * NR + q] = u.e;
-  R[4 * NR + q] = u.mx * inv2a;
-  R[5 * NR + q] = (u.mx * v1 + p) * inv2a;
-  R[6 * NR + q] = (u.my * v1) * inv2a;
-  R[7 * NR + q] = ((u.e + p) * v1) * inv2a;
-  R[8 * NR + q] = u.my * inv2a;
-  R[9 * NR + q] = (u.mx * v2) * inv2a;
-  R[10 * NR + q] = (u.my * v2 + p) * inv2a;
-  R[11 * NR + q] = ((u.e + p) * v2) * inv2a;
-  R[12 * NR + q] = p;
-}
-
-__device__ __forceinline__ cs staged_u(const double* R, int NR, int q) {
-  return {R[q], R[NR + q], R[2 * NR + q], R[3 * NR + q]};
-}
-
-// M_k of a staged cell: w*u + inv2a*f (k=0), w*u - inv2a*f (1), +/- inv2a*g (2, 3).
-__device__ __forceinline__ cs staged_m(const double* R, int NR, int q, int k, double w) {
-  const cs wu = scale(w, staged_u(R, NR, q));
-  const int b = (k < 2 ? 4 : 8) * NR;
-  const cs a = {R[b + q], R[b + NR + q], R[b + 2 * NR + q], R[b + 3 * NR + q]};
-  return (k & 1) ? sub(wu, a) : add(wu, a);
-}
-
-__device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
-
-// Population k at padded (i, j); interior cells take the direct path.
-__device__ __forceinline__ cs pop_at(const MarchParams& P, const double* src, const double* rows,
-                                     int k, int i, int j, double inv2a) {
-  if (i >= 0 && i < P.nx && j >= 0 && j < P.ny)
-    return load_plane4(src + (4 + 4 * k) * P.plane, P.plane, (long long)j * P.pitch + i);
-  return load_pop(P, src, rows, k, i, j, inv2a);
-}
-
-__global__ void __launch_bounds__(tiled::NT, 2) k_theta_tiled(MarchParams P, int tiles_x) {
-  using namespace tiled;
-  extern __shared__ double sm[];
-  __shared__ int qn;
-  const int s = blockIdx.y;
-  const SampleCtl* c = P.ctl + s;
-  if (!c->active) return;
-  double* R = sm;                     // kStaged x NR2
-  double* RF = R + kStaged * NR2;     // rfo[NF], pfo[NF]
-  double* Q = RF + 2 * NF;            // hard-cell queue, QW x NT (SoA)
-  int* qidx = reinterpret_cast<int*>(Q + QW * NT);
-  const int x0 = (blockIdx.x % tiles_x) * TX, y0 = (blockIdx.x / tiles_x) * TY;
-  const double* src = state_src(P, s, c->parity);
-  const double* rows = P.inlet + (long long)s * P.ny * 4;
-  const double inv2a = 0.5 / c->a;
-  const double gm1 = P.gm1, w = P.w, al = P.alpha;
-  if (threadIdx.x == 0) qn = 0;
-
-  // Phase 1: stage u, fluxes and p(u) on the tile + halo 2.
-  for (int q = threadIdx.x; q < NR2; q += NT) {
-    const int gi = clampi(x0 + q % RX2 - 2, -2, P.nx + 1);
-    const int gj = clampi(y0 + q / RX2 - 2, -2, P.ny + 1);
-    stage_cell(R, NR2, q, load_u(P, src, rows, gi, gj), inv2a, gm1);
-  }
-  __syncthreads();
-
-  // Phase 2: first-order candidates (compute_candidates, solver.hpp:301-316)
-  // on the tile and its 1-ring (corners are never used).
-  auto rq = [](int x, int y) { return (y + 2) * RX2 + (x + 2); };
-  auto fq = [](int x, int y) { return (y + 1) * FX + (x + 1); };
-  auto ufo_at = [&](int x, int y) {
-    const cs a = add(staged_m(R, NR2, rq(x - 1, y), 0, w), staged_m(R, NR2, rq(x + 1, y), 1, w));
-    const cs b = add(staged_m(R, NR2, rq(x, y - 1), 2, w), staged_m(R, NR2, rq(x, y + 1), 3, w));
-    return add(add(a, b), scale(al, staged_u(R, NR2, rq(x, y))));
-  };
-  const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
-  const cs foC = ufo_at(tx, ty);
-  RF[fq(tx, ty)] = foC.r;
-  RF[NF + fq(tx, ty)] = pressure(foC, gm1);
-  if (threadIdx.x < 2 * TX + 2 * TY) {
-    const int t = threadIdx.x;
-    int x, y;
-    if (t < TX) {
-      x = t, y = -1;
-    } else if (t < 2 * TX) {
-      x = t - TX, y = TY;
-    } else if (t < 2 * TX + TY) {
-      x = -1, y = t - 2 * TX;
-    } else {
-      x = TX, y = t - 2 * TX - TY;
-    }
-    const cs fo = ufo_at(x, y);
-    RF[fq(x, y)] = fo.r;
-    RF[NF + fq(x, y)] = pressure(fo, gm1);
-  }
-  __syncthreads();
-
-  // Phase 3: gather the limiter inputs of this thread's cell and try theta = 1.
-  const int i = x0 + tx, j = y0 + ty;
-  const bool valid = i < P.nx && j < P.ny;
-  if (valid) {
-    cs cf[4];
-    {
-      const cs P0W = pop_at(P, src, rows, 0, i - 1, j, inv2a);
-      const cs P1E = pop_at(P, src, rows, 1, i + 1, j, inv2a);
-      const cs P2S = pop_at(P, src, rows, 2, i, j - 1, inv2a);
-      const cs P3N = pop_at(P, src, rows, 3, i, j + 1, inv2a);
-      const long long off = (long long)j * P.pitch + i;
-      const cs P0C = load_plane4(src + 4 * P.plane, P.plane, off);
-      const cs P1C = load_plane4(src + 8 * P.plane, P.plane, off);
-      const cs P2C = load_plane4(src + 12 * P.plane, P.plane, off);
-      const cs P3C = load_plane4(src + 16 * P.plane, P.plane, off);
-      const int qc = rq(tx, ty);
-      cf[0] = sub(sub(staged_m(R, NR2, rq(tx - 1, ty), 0, w), P0W),
-                  sub(staged_m(R, NR2, qc, 1, w), P1C));
-      cf[1] = sub(sub(staged_m(R, NR2, rq(tx + 1, ty), 1, w), P1E),
-                  sub(staged_m(R, NR2, qc, 0, w), P0C));
-      cf[2] = sub(sub(staged_m(R, NR2, rq(tx, ty - 1), 2, w), P2S),
-                  sub(staged_m(R, NR2, qc, 3, w), P3C));
-      cf[3] = sub(sub(staged_m(R, NR2, rq(tx, ty + 1), 3, w), P3N),
-                  sub(staged_m(R, NR2, qc, 2, w), P2C));
-    }
-    RlmpStencil st;
-    st.fo = foC;
-    const int fpts[5] = {fq(tx, ty), fq(tx - 1, ty), fq(tx + 1, ty), fq(tx, ty - 1), fq(tx, ty + 1)};
-#pragma unroll
-    for (int n = 0; n < 5; ++n) {
-      st.rfo[n] = RF[fpts[n]];
-      st.pfo[n] = RF[NF + fpts[n]];
-    }
-    const int rpts[9] = {rq(tx, ty),     rq(tx - 1, ty), rq(tx + 1, ty), rq(tx, ty - 1), rq(tx, ty + 1),
-                         rq(tx - 2, ty), rq(tx + 2, ty), rq(tx, ty - 2), rq(tx, ty + 2)};
-#pragma unroll
-    for (int n = 0; n < 9; ++n) {
-      st.rprev[n] = R[rpts[n]];
-      st.pprev[n] = R[12 * NR2 + rpts[n]];
-    }
-    const RlmpBounds b = rlmp_bounds(st, P.kappa, P.rho_floor_coef, P.p_floor_coef);
-    const cs delta = add(add(cf[0], cf[1]), add(cf[2], cf[3]));
-    if (feasible(1.0, foC, delta, cf, b, gm1)) {
-      P.theta[(long long)s * P.plane + (long long)j * P.pitch + i] = 1.0;
-    } else {
-      const int slot = atomicAdd(&qn, 1);
-      Q[0 * NT + slot] = foC.r;
-      Q[1 * NT + slot] = foC.mx;
-      Q[2 * NT + slot] = foC.my;
-      Q[3 * NT + slot] = foC.e;
-#pragma unroll
-      for (int f = 0; f < 4; ++f) {
-        Q[(4 + 4 * f) * NT + slot] = cf[f].r;
-        Q[(5 + 4 * f) * NT + slot] = cf[f].mx;
-        Q[(6 + 4 * f) * NT + slot] = cf[f].my;
-        Q[(7 + 4 * f) * NT + slot] = cf[f].e;
-      }
-      Q[20 * NT + slot] = b.rho_lo;
-      Q[21 * NT + slot] = b.rho_hi;
-      Q[22 * NT + slot] = b.p_lo;
-      Q[23 * NT + slot] = b.p_hi;
-      qidx[slot] = j * P.pitch + i;
-    }
-  }
-  __syncthreads();
-
-  // Phase 4: the cells that failed theta = 1 go to the global hard-cell queue
-  // (one atomic per CTA), processed by k_theta_hard at full occupancy so the
-  // 30-step bisections neither serialise warps of easy cells nor keep this
-  // CTA resident.  If the queue is full they are finished here instead.
-  const int n = qn;
-  if (n == 0) return;
-  __shared__ int qbase;
-  if (threadIdx.x == 0) qbase = P.hq ? atomicAdd(P.hq_n, n) : P.hq_cap;
-  __syncthreads();
-  const int base = qbase;
-  if (base + n <= P.hq_cap) {
-    for (int slot = threadIdx.x; slot < n; slot += NT) {
-#pragma unroll 4
-      for (int k = 0; k < kHardWords; ++k)
-        P.hq[(long long)k * P.hq_cap + base + slot] = Q[k * NT + slot];
-      P.hq_idx[base + slot] = (long long)s * P.plane + qidx[slot];
-    }
-    return;
-  }
-  for (int slot = base + threadIdx.x; slot < P.hq_cap; slot += NT) P.hq_idx[slot] = -1;
-  for (int slot = threadIdx.x; slot < n; slot += NT) {
-    const cs fo = {Q[0 * NT + slot], Q[1 * NT + slot], Q[2 * NT + slot], Q[3 * NT + slot]};
-    cs cf[4];
-#pragma unroll
-    for (int f = 0; f < 4; ++f)
-      cf[f] = {Q[(4 + 4 * f) * NT + slot], Q[(5 + 4 * f) * NT + slot], Q[(6 + 4 * f) * NT + slot],
-               Q[(7 + 4 * f) * NT + slot]};
-    RlmpBounds b;
-    b.rho_lo = Q[20 * NT + slot];
-    b.rho_hi = Q[21 * NT + slot];
-    b.p_lo = Q[22 * NT + slot];
-    b.p_hi = Q[23 * NT + slot];
-    b.rho_floor = P.rho_floor_coef;
-    b.p_floor = P.p_floor_coef;
-    const double th = rlmp_theta_hard(fo, cf, b, gm1);
-    P.theta[(long long)s * P.plane + qidx[slot]] = th;
-  }
-}
-
-// The limiter's hard cells from the global queue (rlmp_theta after a failed
-// feasible(1.0), solver.hpp:462-486), one thread per cell, grid-stride.
-__global__ void __launch_bounds__(256, 2) k_theta_hard(MarchParams P) {
-  const int n = min(*P.hq_n, P.hq_cap);
-  const long long cap = P.hq_cap;
-  for (int slot = blockIdx.x * blockDim.x + threadIdx.x; slot < n;
-       slot += gridDim.x * blockDim.x) {
-    const long long idx = P.hq_idx[slot];
-    if (idx < 0) continue;
-    const double* q = P.hq + slot;
-    const cs fo = {q[0], q[cap], q[2 * cap], q[3 * cap]};
-    cs cf[4];
-#pragma unroll
-    for (int f = 0; f < 4; ++f)
-      cf[f] = {q[(4 + 4 * f) * cap], q[(5 + 4 * f) * cap], q[(6 + 4 * f) * cap],
-               q[(7 + 4 * f) * cap]};
-    RlmpBounds b;
-    b.rho_lo = q[20 * cap];
-    b.rho_hi = q[21 * cap];
-    b.p_lo = q[22 * cap];
-    b.p_hi = q[23 * cap];
-    b.rho_floor = P.rho_floor_coef;
-    b.p_floor = P.p_floor_coef;
-    P.theta[idx] = rlmp_theta_hard(fo, cf, b, P.gm1);
-  }
-}
-
-// Blended stream-collide, tiled: M_k of the tile + 1-ring from shared memory.
-template <int kMode>
-__global__ void __launch_bounds__(tiled::NT, 2) k_advance_tiled(MarchParams P, double const_theta,
-                                                                int tiles_x) {
-  using namespace tiled;
-  extern __shared__ double sm[];
-  const int s = blockIdx.y;
-  SampleCtl* c = P.ctl + s;
-  if (!c->active) return;
-  double* R = sm;
-  const int x0 = (blockIdx.x % tiles_x) * TX, y0 = (blockIdx.x / tiles_x) * TY;
-  const double* src = state_src(P, s, c->parity);
-  double* dst = state_dst(P, s, c->parity);
-  const double* rows = P.inlet + (long long)s * P.ny * 4;
-  const double inv2a = 0.5 / c->a;
-  const double gm1 = P.gm1, w = P.w;
-  for (int q = threadIdx.x; q < NR1; q += NT) {
-    const int gi = clampi(x0 + q % RX1 - 1, -2, P.nx + 1);
-    const int gj = clampi(y0 + q / RX1 - 1, -2, P.ny + 1);
-    stage_cell(R, NR1, q, load_u(P, src, rows, gi, gj), inv2a, gm1);
-  }
-  __syncthreads();
-  const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
-  const int i = x0 + tx, j = y0 + ty;
-  unsigned long long bits = 0;
-  int bad = 0, nonfin = 0;
-  if (i < P.nx && j < P.ny) {
-    auto rq = [](int x, int y) { return (y + 1) * RX1 + (x + 1); };
-    double tw, te, ts, tn;
-    face_thetas<kMode>(P, s, i, j, const_theta, tw, te, ts, tn);
-    const long long off = (long long)j * P.pitch + i;
-    const int qc = rq(tx, ty);
-    const cs M0W = staged_m(R, NR1, rq(tx - 1, ty), 0, w);
-    const cs M1E = staged_m(R, NR1, rq(tx + 1, ty), 1, w);
-    const cs M2S = staged_m(R, NR1, rq(tx, ty - 1), 2, w);
-    const cs M3N = staged_m(R, NR1, rq(tx, ty + 1), 3, w);
-    const cs n1 = add(M0W, scale(tw, sub(M0W, pop_at(P, src, rows, 0, i - 1, j, inv2a))));
-    const cs n2 = add(M1E, scale(te, sub(M1E, pop_at(P, src, rows, 1, i + 1, j, inv2a))));
-    const cs n3 = add(M2S, scale(ts, sub(M2S, pop_at(P, src, rows, 2, i, j - 1, inv2a))));
-    const cs n4 = add(M3N, scale(tn, sub(M3N, pop_at(P, src, rows, 3, i, j + 1, inv2a))));
-    store_plane4(dst + 4 * P.plane, P.plane, off, n1);
-    store_plane4(dst + 8 * P.plane, P.plane, off, n2);
-    store_plane4(dst + 12 * P.plane, P.plane, off, n3);
-    store_plane4(dst + 16 * P.plane, P.plane, off, n4);
-    const cs P0C = load_plane4(src + 4 * P.plane, P.plane, off);
-    const cs P1C = load_plane4(src + 8 * P.plane, P.plane, off);
-    const cs P2C = load_plane4(src + 12 * P.plane, P.plane, off);
-    const cs P3C = load_plane4(src + 16 * P.plane, P.plane, off);
-    cs un = add(add(add(n1, n2), add(n3, n4)), scale(P.alpha, staged_u(R, NR1, qc)));
-    const cs out = add(add(scale(tw, sub(staged_m(R, NR1, qc, 1, w), P1C)),
-                           scale(te, sub(staged_m(R, NR1, qc, 0, w), P0C))),
-                       add(scale(ts, sub(staged_m(R, NR1, qc, 3, w), P3C)),
-                           scale(tn, sub(staged_m(R, NR1, qc, 2, w), P2C))));
-    un = sub(un, out);
-    store_plane4(dst, P.plane, off, un);
-    const double sp = signal_speed(un, P.gamma, gm1, P.conservative);
-    if (!isfinite(sp))
-      bad = 1;
-    else
-      bits = (unsigned long long)__double_as_longlong(sp);
-    nonfin = !finite4(un);
-  }
-  reduce_signal(c, bits, bad, nonfin);
-}
-
-template __global__ void k_advance_tiled<0>(MarchParams, double, int);
-template __global__ void k_advance_tiled<1>(MarchParams, double, int);
-template __global__ void k_advance_tiled<2>(MarchParams, double, int);
 
 }  // namespace vlbm_dev
 
@@ -881,40 +380,12 @@ static bool use_v0() {
   return v != 0;
 }
 
-static cudaError_t smem_attrs() {
-  static cudaError_t done = [] {
-    cudaError_t e = cudaFuncSetAttribute(k_theta_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)tiled::kThetaSmem);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_advance_tiled<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)tiled::kAdvanceSmem);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_advance_tiled<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)tiled::kAdvanceSmem);
-    if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_advance_tiled<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)tiled::kAdvanceSmem);
-  }();
-  return done;
-}
-
-static dim3 tiled_grid(const MarchParams& P, int& tiles_x) {
-  tiles_x = (P.nx + tiled::TX - 1) / tiled::TX;
-  const int ty = (P.ny + tiled::TY - 1) / tiled::TY;
-  return dim3(tiles_x * ty, P.S);
-}
-
 cudaError_t launch_theta(const MarchParams& P, cudaStream_t st) {
   if (use_v0()) {
     k_theta<<<tile_grid(P), 256, 0, st>>>(P);
     return cudaGetLastError();
   }
-  if (cudaError_t e = smem_attrs()) return e;
-  int tx;
-  const dim3 g = tiled_grid(P, tx);
-  k_theta_tiled<<<g, tiled::NT, tiled::kThetaSmem, st>>>(P, tx);
-  if (P.hq) k_theta_hard<<<148 * 8, 256, 0, st>>>(P);
-  return cudaGetLastError();
+  return launch_theta_tiled(P, st);
 }
 
 cudaError_t launch_advance(const MarchParams& P, int mode, double const_theta, cudaStream_t st) {
@@ -928,17 +399,7 @@ cudaError_t launch_advance(const MarchParams& P, int mode, double const_theta, c
       k_advance<2><<<g, 256, 0, st>>>(P, const_theta);
     return cudaGetLastError();
   }
-  if (cudaError_t e = smem_attrs()) return e;
-  int tx;
-  const dim3 g = tiled_grid(P, tx);
-  const size_t sm = tiled::kAdvanceSmem;
-  if (mode == 0)
-    k_advance_tiled<0><<<g, tiled::NT, sm, st>>>(P, const_theta, tx);
-  else if (mode == 1)
-    k_advance_tiled<1><<<g, tiled::NT, sm, st>>>(P, const_theta, tx);
-  else
-    k_advance_tiled<2><<<g, tiled::NT, sm, st>>>(P, const_theta, tx);
-  return cudaGetLastError();
+  return launch_advance_tiled(P, mode, const_theta, st);
 }
 
 cudaError_t launch_set_budget(const MarchParams& P, long long budget, cudaStream_t st) {

@@ -21,6 +21,8 @@ enum { LIM_FIRST = 0, LIM_SECOND = 1, LIM_RLMP = 2 };
 enum { ST_RUNNING = 0, ST_DIVERGED = 2 };
 constexpr int kPlanes = 20;
 constexpr int kHardWords = 24;  // u_FO (4), c_w/c_e/c_s/c_n (16), rho_lo/hi, p_lo/hi
+constexpr int kBisWords = 13;
+constexpr int kUncWords = 28;
 
 // Per-sample control block.  Written by k_sched (one thread per sample) and
 // by the advance epilogue (atomics on smax_bits / flags).
@@ -57,7 +59,17 @@ struct MarchParams {
   double* hq;
   long long* hq_idx;  // s * plane + j * pitch + i
   int* hq_n;
+  int* hq_next;  // unused slot (hq_n[1]); hq_n[2], hq_n[3]: bisection queue counts
   int hq_cap;
+  // Bisection queues (capacity hq_cap each), filled by k_theta_hard:
+  //   bq: vertices all certified -- u_FO(4), delta(4), rho_lo/hi, p_lo/hi, thc  (kBisWords)
+  //   cq: some uncertified -- u_FO(4), c_f(16), rho_lo/hi, p_lo/hi, thc, p0, err, er (kUncWords)
+  //   *_idx: cell index; cq_idx packs the uncertified-vertex mask in bits 40..55
+  double* bq;
+  long long* bq_idx;
+  double* cq;
+  long long* cq_idx;
+  int* audit;    // optional: disagreements of the certified bisection (must stay 0)
   double dx, gamma, gm1, alpha, w, safety, kappa, rho_floor_coef, p_floor_coef;
   double rho_ref, p_ref;
   int bc[4];

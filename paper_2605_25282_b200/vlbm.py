@@ -182,6 +182,8 @@ def lib() -> C.CDLL:
     sig("vlbm_batch_stream", V, [V])
     sig("vlbm_batch_set_timing", I, [V, I])
     sig("vlbm_batch_stats", I, [V, C.POINTER(I64), DP, DP, DP, C.POINTER(I64)])
+    sig("vlbm_batch_set_audit", I, [V, I])
+    sig("vlbm_batch_audit", I, [V, C.POINTER(I64)])
     sig("vlbm_restrict_field", I, [I, I, DP, DP])
     sig("vlbm_strong_error", I, [I, I64, DP, DP, DP, DP])
     sig("vlbm_wasserstein1", I, [I, I64, DP, DP, I, DP])
@@ -373,6 +375,18 @@ class BatchSimulation:
                                       C.byref(ms), C.byref(cu)))
         return dict(launches=la.value, ms_theta=mt.value, ms_advance=ma.value,
                     ms_sched=ms.value, cell_updates=cu.value)
+
+    def set_audit(self, on: bool = True) -> None:
+        """Re-check every certified bisection step with the full feasible()."""
+        _check(lib().vlbm_batch_set_audit(self._h, int(on)))
+
+    def audit_counters(self) -> dict:
+        n = (I64 * 4)()
+        _check(lib().vlbm_batch_audit(self._h, n))
+        return dict(mismatches=n[0], bisections=n[1], certified=n[2], vertex_fail_at_thc=n[3])
+
+    def audit_mismatches(self) -> int:
+        return self.audit_counters()["mismatches"]
 
     def device_u(self, s: int = 0) -> int:
         p = DP()
