@@ -105,7 +105,8 @@ def dist_env():
     return ws, rank, local
 
 
-def cpu_reference(args, n_gpus, threads=None, seconds=15.0):
+def cpu_reference(args, n_gpus, threads=None, seconds=None):
+    seconds = seconds or getattr(args, "ref_seconds", 15.0)
     """The reference CPU march (oracle/_ref = the unmodified reference
     headers) on this host's cores: one sample per thread, run_ensemble-style
     task pool, file I/O excluded; a bounded sample of the same workload
@@ -235,6 +236,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-postproc", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--ref-seconds", type=float, default=15.0,
+                    help="target CPU seconds of the reference-CPU sample")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)

@@ -17,7 +17,9 @@ def oc():
 
 
 def bits(a):
-    return np.ascontiguousarray(a, np.float64).view(np.uint64)
+    a = np.array(a, np.float64)
+    a[np.isnan(a)] = np.nan
+    return a.view(np.uint64)
 
 
 def ens(rng, M, ny, nx, ties=False):
