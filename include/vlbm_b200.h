@@ -144,6 +144,13 @@ int vlbm_inlet_rows(const vlbm_grid* g, const vlbm_perturbation* pp, double gamm
 int vlbm_batch_create(const vlbm_grid* g, const vlbm_params* p, const vlbm_perturbation* pp,
                       uint64_t base_seed, int64_t m0, int n_samples, double strip_width,
                       int device, vlbm_batch** out);
+/* Jet-case batch from explicit mode coefficients (SampleSpec::coeffs,
+ * solver.hpp:611-619; e.g. read back from a manifest): y_coeffs, z_coeffs
+ * are n_samples x pp->modes; seeds (ModeCoefficients::seed) may be NULL. */
+int vlbm_batch_create_coeffs(const vlbm_grid* g, const vlbm_params* p,
+                             const vlbm_perturbation* pp, int n_samples, const double* y_coeffs,
+                             const double* z_coeffs, double strip_width, int device,
+                             vlbm_batch** out);
 /* Generic batch on caller-provided initial fields (n_samples field blocks)
  * and optional inlet rows (n_samples x ny x 4; required iff bc[0] is
  * Inlet).  seeds may be NULL. */

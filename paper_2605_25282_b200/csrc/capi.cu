@@ -309,6 +309,22 @@ int vlbm_batch_create(const vlbm_grid* g, const vlbm_params* p, const vlbm_pertu
                       int device, vlbm_batch** out) {
   if (!pp) return set_error(VLBM_E_INVALID, "null perturbation");
   if (int rc = vlbm_impl::validate_perturbation(*pp)) return rc;
+  if (n_samples < 1) return set_error(VLBM_E_INVALID, "n_samples must be >= 1");
+  const int K = pp->modes;
+  std::vector<double> yc((size_t)K * n_samples), zc((size_t)K * n_samples);
+  for (int s = 0; s < n_samples; ++s)
+    vlbm_draw_coefficients(base_seed, (uint64_t)(m0 + s), K, yc.data() + (size_t)K * s,
+                           zc.data() + (size_t)K * s);
+  return vlbm_batch_create_coeffs(g, p, pp, n_samples, yc.data(), zc.data(), strip_width, device,
+                                  out);
+}
+
+int vlbm_batch_create_coeffs(const vlbm_grid* g, const vlbm_params* p,
+                             const vlbm_perturbation* pp, int n_samples, const double* y_all,
+                             const double* z_all, double strip_width, int device,
+                             vlbm_batch** out) {
+  if (!pp || !y_all || !z_all) return set_error(VLBM_E_INVALID, "null argument");
+  if (int rc = vlbm_impl::validate_perturbation(*pp)) return rc;
   if (strip_width < 0.0) return set_error(VLBM_E_INVALID, "config: inlet_strip_width must be >= 0");
   // run_sample's construction (solver.hpp:633-640): jet boundaries and
   // set_reference(rho_amb, p_amb).
@@ -322,7 +338,7 @@ int vlbm_batch_create(const vlbm_grid* g, const vlbm_params* p, const vlbm_pertu
   vlbm_batch* b = nullptr;
   if (int rc = alloc_batch(g, &q, n_samples, device, &b)) return rc;
   const int K = pp->modes;
-  std::vector<double> yc(K), zc(K), rows(4 * (size_t)g->ny);
+  std::vector<double> rows(4 * (size_t)g->ny);
   double* field = nullptr;
   const size_t n = (size_t)g->nx * g->ny;
   if (cudaMallocHost(&field, sizeof(double) * 4 * n) != cudaSuccess) {
@@ -331,11 +347,12 @@ int vlbm_batch_create(const vlbm_grid* g, const vlbm_params* p, const vlbm_pertu
   }
   int rc = VLBM_OK;
   for (int s = 0; s < n_samples && rc == VLBM_OK; ++s) {
-    vlbm_draw_coefficients(base_seed, (uint64_t)(m0 + s), K, yc.data(), zc.data());
+    const double* yc = y_all + (size_t)K * s;
+    const double* zc = z_all + (size_t)K * s;
     for (int j = 0; j < g->ny; ++j)
-      vlbm_impl::inlet_state(vlbm_impl::y_center(*g, j), K, yc.data(), zc.data(), *pp, q.gamma,
+      vlbm_impl::inlet_state(vlbm_impl::y_center(*g, j), K, yc, zc, *pp, q.gamma,
                              rows.data() + 4 * j);
-    vlbm_impl::initial_field(*g, K, yc.data(), zc.data(), *pp, q.gamma, strip_width, field);
+    vlbm_impl::initial_field(*g, K, yc, zc, *pp, q.gamma, strip_width, field);
     rc = upload_sample(b, s, field, rows.data());
     if (rc == VLBM_OK && cudaStreamSynchronize(b->stream) != cudaSuccess)
       rc = set_error(VLBM_E_CUDA, "upload");
