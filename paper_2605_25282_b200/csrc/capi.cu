@@ -115,7 +115,7 @@ int alloc_batch(const vlbm_grid* g, const vlbm_params* p, int S, int device, vlb
   MarchParams& P = b->P;
   P.nx = g->nx;
   P.ny = g->ny;
-  P.pitch = g->nx;
+  P.pitch = (g->nx + 15) / 16 * 16;  // 128-byte rows: TMA strides and coalescing
   P.S = S;
   P.plane = (long long)P.ny * P.pitch;
   P.sample_stride = vlbm_dev::kPlanes * P.plane;
@@ -182,6 +182,7 @@ int alloc_batch(const vlbm_grid* g, const vlbm_params* p, int S, int device, vlb
       if (rc == VLBM_OK) chk(cudaMemset(P.hq_n, 0, 4 * sizeof(int)), "memset hq_n");
     }
   }
+  if (rc == VLBM_OK) rc = vlbm_impl::encode_tensor_maps(P);
   if (rc == VLBM_OK) {
     chk(cudaMemsetAsync(P.buf0, 0, state_bytes, b->stream), "memset");
     chk(cudaMemsetAsync(P.buf1, 0, state_bytes, b->stream), "memset");

@@ -38,6 +38,7 @@ cudaError_t launch_theta(const vlbm_dev::MarchParams& P, cudaStream_t st);
 cudaError_t launch_advance(const vlbm_dev::MarchParams& P, int mode, double const_theta,
                            cudaStream_t st);
 // tiled production kernels (march_tiled.cu)
+int encode_tensor_maps(vlbm_dev::MarchParams& P);
 cudaError_t launch_theta_tiled(const vlbm_dev::MarchParams& P, cudaStream_t st);
 cudaError_t launch_advance_tiled(const vlbm_dev::MarchParams& P, int mode, double const_theta,
                                  cudaStream_t st);

@@ -10,6 +10,8 @@
 // No ghost cells are stored: the boundary ring is synthesised on load from
 // the interior (fill_ghosts semantics, solver.hpp:230-286).
 #pragma once
+#include <cuda.h>
+
 #include <cstdint>
 
 #include "vlbm_device.cuh"
@@ -70,6 +72,9 @@ struct MarchParams {
   double* cq;
   long long* cq_idx;
   int* audit;    // optional: disagreements of the certified bisection (must stay 0)
+  // TMA tensor maps [x, y, plane, sample] of buffer 0/1 with the tile boxes of
+  // the advance (34x10x20), the limiter's u (36x12x4) and populations (34x10x16).
+  CUtensorMap tm_adv[2], tm_thu[2], tm_thp[2];
   double dx, gamma, gm1, alpha, w, safety, kappa, rho_floor_coef, p_floor_coef;
   double rho_ref, p_ref;
   int bc[4];

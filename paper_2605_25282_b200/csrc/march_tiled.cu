@@ -1,24 +1,26 @@
 // march_tiled.cu — the production march kernels for sm_100a.
 //
 // A CTA owns a TX x TY tile of interior cells of one sample (blockIdx.y), one
-// thread per cell.  Every global value the tile needs is fetched ONCE into
-// shared memory with cp.async (LDGSTS, all loads of the tile in flight at
-// once): the macroscopic state on the tile + halo (2 for the limiter, 1 for
-// the advance) and the four streamed populations on the tile + the one-cell
-// ring each of them is pulled from.  Boundary tiles synthesise the ghost ring
-// while staging (fill_ghosts semantics, march_common.cuh).  From the staged u
-// each halo cell's inv2a*f(u), inv2a*g(u) and p(u) are formed once, so every
-// flux / pressure division is evaluated once per cell; M_k(u) is rebuilt from
-// them exactly as maxwellians() forms it (w*u +/- inv2a*f, lattice.hpp:43-55),
-// hence bit-identical to the reference.
+// thread per cell.  The tile's inputs arrive in shared memory by TMA
+// (cp.async.bulk.tensor, 4-D tensor maps over [sample][plane][y][x] of each
+// state buffer, completion on an mbarrier): ONE bulk copy of the 20 state
+// planes on the tile + 1-ring for the advance; for the limiter, u on the tile
+// + 2-ring and the 16 population planes on the tile + 1-ring.  Boundary
+// tiles then overwrite the out-of-domain cells of the staged box with the
+// ghost values of the reference's fill_ghosts (march_common.cuh::resolve).
+// From the staged u each cell's inv2a*f(u), inv2a*g(u) and p(u) are formed
+// once, so every flux / pressure division is evaluated once per cell; M_k(u)
+// is rebuilt from them exactly as maxwellians() forms it (w*u +/- inv2a*f,
+// lattice.hpp:43-55), hence bit-identical to the reference.
 //
 //   k_theta_tiled   u_FO, rlmp_bounds, feasible(1) per cell; cells that fail
 //                   it (the limiter's hard cells) are appended to a global
 //                   queue (warp-aggregated slots, one atomic per CTA)
-//   k_theta_hard    the rest of rlmp_theta for the queued cells at full
-//                   occupancy (solver.hpp:462-486)
+//   k_theta_hard / k_bisect_cert / k_bisect_unc
+//                   the rest of rlmp_theta for the queued cells
 //   k_advance_tiled blended pull stream-collide (solver.hpp:536-575) + the
 //                   per-sample kinetic-speed / finiteness epilogue
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "internal.h"
@@ -29,31 +31,53 @@
 namespace vlbm_dev {
 namespace tiled {
 constexpr int TX = 32, TY = 8, NT = TX * TY;
-// population staging: P0 on x in [-1,TX), P1 on x in [0,TX], P2 on y in
-// [-1,TY), P3 on y in [0,TY]  (the pull sources of the tile, plus the tile)
-constexpr int NPX = (TX + 1) * TY;      // 264
-constexpr int NPY = TX * (TY + 1);      // 288
-constexpr int NPC = 2 * NPX + 2 * NPY;  // per component
-constexpr int NPOP = 4 * NPC;           // 4416 doubles
-constexpr int RX2 = TX + 4, RY2 = TY + 4, NR2 = RX2 * RY2;  // limiter region (halo 2)
-constexpr int FX = TX + 2, FY = TY + 2, NF = FX * FY;       // u_FO region (ring 1)
-constexpr int RX1 = TX + 2, RY1 = TY + 2, NR1 = RX1 * RY1;  // advance region (halo 1)
-constexpr int kStagedTheta = 13;  // u(4), inv2a*f(4), inv2a*g(4), p
-constexpr int kStagedAdv = 12;    // u(4), inv2a*f(4), inv2a*g(4)
-constexpr size_t kThetaSmem = sizeof(double) * (kStagedTheta * NR2 + 2 * NF + NPOP);
-constexpr size_t kAdvanceSmem = sizeof(double) * (kStagedAdv * NR1 + NPOP);
+constexpr int RX2 = TX + 4, RY2 = TY + 4, NR2 = RX2 * RY2;  // limiter u box (halo 2): 36 x 12
+constexpr int RX1 = TX + 2, RY1 = TY + 2, NR1 = RX1 * RY1;  // halo-1 box: 34 x 10
+constexpr int FX = RX1, NF = NR1;                           // u_FO ring region
+// TMA boxes start at an even x (16-byte aligned for 8-byte elements; an odd
+// origin faults): the halo-1 boxes are loaded from x0-2, 36 wide.
+constexpr int AX = TX + 4, AY = TY + 2, NA = AX * AY;        // 36 x 10
+constexpr int kStagedTheta = 13;  // u(4) [TMA], inv2a*f(4), inv2a*g(4), p
+// limiter smem: R [13][NR2] | RF [2][NF] | pad | SP [16][NA] (TMA, 128-B aligned)
+constexpr int kThetaSP = ((kStagedTheta * NR2 + 2 * NF) + 15) / 16 * 16;
+constexpr size_t kThetaSmem = sizeof(double) * (kThetaSP + 16 * NA);
+constexpr unsigned kThetaTx = sizeof(double) * (4 * NR2 + 16 * NA);
+// advance smem: R [20][NA] (TMA: u + pops) | F [8][NA] (inv2a f, inv2a g)
+constexpr int kAdvF = 20 * NA;
+constexpr size_t kAdvanceSmem = sizeof(double) * (kAdvF + 8 * NA);
+constexpr unsigned kAdvanceTx = sizeof(double) * 20 * NA;
 }  // namespace tiled
 
-__device__ __forceinline__ void cp_async8(double* dst_smem, const double* src) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(dst_smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src) : "memory");
+// ---- TMA + mbarrier (PTX) -----------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
 }
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;\n" ::: "memory");
+__device__ __forceinline__ void mbar_init(unsigned long long* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
 }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+// 4-D tile [x, y, plane, sample] -> shared memory, OOB elements zero-filled.
+__device__ __forceinline__ void tma_load_4d(double* dst, const CUtensorMap* map,
+                                            unsigned long long* bar, int x, int y, int p, int s) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];\n" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(p), "r"(s)
+      : "memory");
 }
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) {
@@ -62,165 +86,125 @@ __device__ __forceinline__ int clampi(int v, int lo, int hi) {
 __device__ __forceinline__ double comp(const cs& v, int c) {
   return c == 0 ? v.r : (c == 1 ? v.mx : (c == 2 ? v.my : v.e));
 }
+__device__ __forceinline__ bool in_domain(const MarchParams& P, int i, int j) {
+  return i >= 0 && i < P.nx && j >= 0 && j < P.ny;
+}
 
-// Stage component c of u at padded (gi, gj) into *dst.
-__device__ __forceinline__ void stage_u_elem(const MarchParams& P, const double* src,
-                                             const double* rows, int gi, int gj, int c,
-                                             double* dst, bool interior) {
-  if (interior) {
-    cp_async8(dst, src + c * P.plane + (long long)gj * P.pitch + gi);
-    return;
-  }
+// Ghost value of plane `pl` (0..3: u, 4+4k+c: population k component c) at
+// padded (gi, gj): fill_ghosts semantics (solver.hpp:230-286).
+__device__ __forceinline__ double ghost_value(const MarchParams& P, const double* src,
+                                              const double* rows, int pl, int gi, int gj,
+                                              double inv2a) {
   const Src r = resolve(P, clampi(gi, -2, P.nx + 1), clampi(gj, -2, P.ny + 1));
+  const int c = pl < 4 ? pl : (pl - 4) & 3;
   const bool neg = r.mirror && c == 2;
-  if (r.inlet) {
-    const double v = rows[4 * r.j + c];
-    *dst = neg ? -v : v;
-    return;
+  double v;
+  if (pl < 4) {
+    v = r.inlet ? rows[4 * r.j + c] : src[c * P.plane + (long long)r.j * P.pitch + r.i];
+  } else {
+    const int k = (pl - 4) >> 2;
+    const int ks = r.mirror ? (k ^ ((k >> 1) & 1)) : k;  // {0,1,3,2} under the wall mirror
+    v = r.inlet ? comp(maxw_k(inlet_row(rows, r.j), ks, P.w, inv2a, P.gm1), c)
+                : src[(4 + 4 * ks + c) * P.plane + (long long)r.j * P.pitch + r.i];
   }
-  const double* g = src + c * P.plane + (long long)r.j * P.pitch + r.i;
-  if (neg)
-    *dst = -*g;
-  else
-    cp_async8(dst, g);
+  return neg ? -v : v;
 }
 
-// Stage u on the tile + halo H: R[c * NR + q], q = (y + H) * RX + (x + H).
-template <int H>
-__device__ __forceinline__ void issue_u(const MarchParams& P, const double* src,
-                                        const double* rows, int x0, int y0, double* R) {
-  using namespace tiled;
-  constexpr int RX = TX + 2 * H, NR = RX * (TY + 2 * H);
-  const bool interior = x0 >= H && x0 + TX + H <= P.nx && y0 >= H && y0 + TY + H <= P.ny;
-  for (int e = threadIdx.x; e < 4 * NR; e += NT) {
-    const int c = e / NR, q = e - c * NR;
-    stage_u_elem(P, src, rows, x0 + q % RX - H, y0 + q / RX - H, c, R + e, interior);
-  }
-}
-
-// Stage the populations (layout of tiled::NPOP; element e decodes to k, c, x, y).
-__device__ __forceinline__ void issue_pops(const MarchParams& P, const double* src,
-                                           const double* rows, int x0, int y0, double inv2a,
-                                           double* SP) {
-  using namespace tiled;
-  const bool interior = x0 >= 1 && x0 + TX + 1 <= P.nx && y0 >= 1 && y0 + TY + 1 <= P.ny;
-  for (int e = threadIdx.x; e < NPOP; e += NT) {
-    const int c = e / NPC;
-    int r = e - c * NPC, k, x, y;
-    if (r < NPX) {
-      k = 0, y = r / (TX + 1), x = r - y * (TX + 1) - 1;
-    } else if (r < 2 * NPX) {
-      r -= NPX;
-      k = 1, y = r / (TX + 1), x = r - y * (TX + 1);
-    } else if (r < 2 * NPX + NPY) {
-      r -= 2 * NPX;
-      k = 2, y = r / TX - 1, x = r % TX;
-    } else {
-      r -= 2 * NPX + NPY;
-      k = 3, y = r / TX, x = r % TX;
-    }
-    const int gi = x0 + x, gj = y0 + y;
-    if (interior) {
-      cp_async8(SP + e, src + (4 + 4 * k + c) * P.plane + (long long)gj * P.pitch + gi);
-      continue;
-    }
-    const Src s = resolve(P, clampi(gi, -2, P.nx + 1), clampi(gj, -2, P.ny + 1));
-    const int ks = s.mirror ? (k ^ ((k >> 1) & 1)) : k;  // {0,1,3,2} under the wall mirror
-    const bool neg = s.mirror && c == 2;
-    if (s.inlet) {  // inlet ghost populations: M_k(u_in, a) (solver.hpp:236-243)
-      const double v = comp(maxw_k(inlet_row(rows, s.j), ks, P.w, inv2a, P.gm1), c);
-      SP[e] = neg ? -v : v;
-      continue;
-    }
-    const double* g = src + (4 + 4 * ks + c) * P.plane + (long long)s.j * P.pitch + s.i;
-    if (neg)
-      SP[e] = -*g;
-    else
-      cp_async8(SP + e, g);
+// Overwrite the out-of-domain cells of a staged box [planes][RY][RX] whose
+// cell (0, 0) is padded (bx, by) with their ghost values.
+__device__ __forceinline__ void patch_box(const MarchParams& P, const double* src,
+                                          const double* rows, double* box, int RX, int RY, int bx,
+                                          int by, int pl0, int npl, double inv2a) {
+  const int n = RX * RY;
+  for (int e = threadIdx.x; e < n * npl; e += blockDim.x) {
+    const int q = e % n, pl = e / n;
+    const int gi = bx + q % RX, gj = by + q / RX;
+    if (!in_domain(P, gi, gj)) box[e] = ghost_value(P, src, rows, pl0 + pl, gi, gj, inv2a);
   }
 }
 
-// Population k at tile-relative (x, y) from the staged layout.
-__device__ __forceinline__ cs spop(const double* SP, int k, int x, int y) {
-  using namespace tiled;
-  int o;
-  if (k == 0)
-    o = y * (TX + 1) + (x + 1);
-  else if (k == 1)
-    o = NPX + y * (TX + 1) + x;
-  else if (k == 2)
-    o = 2 * NPX + (y + 1) * TX + x;
-  else
-    o = 2 * NPX + NPY + y * TX + x;
-  return {SP[o], SP[NPC + o], SP[2 * NPC + o], SP[3 * NPC + o]};
-}
-
-// inv2a*f(u), inv2a*g(u) and (optionally) p(u) of a staged cell, in place.
-// flux_x/flux_y (euler.hpp:86-97) each evaluate pressure(u): computed once.
-__device__ __forceinline__ void flux_cell(double* R, int NR, int q, double inv2a, double gm1,
-                                          bool with_p) {
-  const cs u = {R[q], R[NR + q], R[2 * NR + q], R[3 * NR + q]};
+// inv2a*f(u), inv2a*g(u) (and p(u)) of one staged cell: u at U[c*NU + q],
+// outputs at F[k*NF + q], k = 0..7 (and p at F[8*NF + q]).  flux_x/flux_y
+// (euler.hpp:86-97) each evaluate pressure(u): computed once.
+__device__ __forceinline__ void flux_cell(const double* U, int NU, double* F, int NFs, int q,
+                                          double inv2a, double gm1, bool with_p) {
+  const cs u = {U[q], U[NU + q], U[2 * NU + q], U[3 * NU + q]};
   const double p = pressure(u, gm1);
   const double v1 = u.mx / u.r;
   const double v2 = u.my / u.r;
-  R[4 * NR + q] = u.mx * inv2a;
-  R[5 * NR + q] = (u.mx * v1 + p) * inv2a;
-  R[6 * NR + q] = (u.my * v1) * inv2a;
-  R[7 * NR + q] = ((u.e + p) * v1) * inv2a;
-  R[8 * NR + q] = u.my * inv2a;
-  R[9 * NR + q] = (u.mx * v2) * inv2a;
-  R[10 * NR + q] = (u.my * v2 + p) * inv2a;
-  R[11 * NR + q] = ((u.e + p) * v2) * inv2a;
-  if (with_p) R[12 * NR + q] = p;
+  F[q] = u.mx * inv2a;
+  F[NFs + q] = (u.mx * v1 + p) * inv2a;
+  F[2 * NFs + q] = (u.my * v1) * inv2a;
+  F[3 * NFs + q] = ((u.e + p) * v1) * inv2a;
+  F[4 * NFs + q] = u.my * inv2a;
+  F[5 * NFs + q] = (u.mx * v2) * inv2a;
+  F[6 * NFs + q] = (u.my * v2 + p) * inv2a;
+  F[7 * NFs + q] = ((u.e + p) * v2) * inv2a;
+  if (with_p) F[8 * NFs + q] = p;
 }
 
-__device__ __forceinline__ cs staged_u(const double* R, int NR, int q) {
-  return {R[q], R[NR + q], R[2 * NR + q], R[3 * NR + q]};
+__device__ __forceinline__ cs plane4(const double* A, int N, int q) {
+  return {A[q], A[N + q], A[2 * N + q], A[3 * N + q]};
 }
 
 // M_k of a staged cell: w*u + inv2a*f (k=0), w*u - inv2a*f (1), +/- inv2a*g (2, 3).
-__device__ __forceinline__ cs staged_m(const double* R, int NR, int q, int k, double w) {
-  const cs wu = scale(w, staged_u(R, NR, q));
-  const int b = (k < 2 ? 4 : 8) * NR;
-  const cs a = {R[b + q], R[b + NR + q], R[b + 2 * NR + q], R[b + 3 * NR + q]};
+__device__ __forceinline__ cs staged_m(const double* U, int NU, const double* F, int NFs, int q,
+                                       int k, double w) {
+  const cs wu = scale(w, plane4(U, NU, q));
+  const cs a = plane4(F + (k < 2 ? 0 : 4 * NFs), NFs, q);
   return (k & 1) ? sub(wu, a) : add(wu, a);
 }
 
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(tiled::NT, 2) k_theta_tiled(MarchParams P, int tiles_x) {
+__global__ void __launch_bounds__(tiled::NT, 2)
+    k_theta_tiled(MarchParams P, int tiles_x, const __grid_constant__ CUtensorMap tmu0,
+                  const __grid_constant__ CUtensorMap tmu1, const __grid_constant__ CUtensorMap tmp0,
+                  const __grid_constant__ CUtensorMap tmp1) {
   using namespace tiled;
-  extern __shared__ double sm[];
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) unsigned long long bar;
   __shared__ int qn, qbase;
   const int s = blockIdx.y;
   const SampleCtl* c = P.ctl + s;
   if (!c->active) return;
-  double* R = sm;                         // kStagedTheta x NR2
-  double* RF = R + kStagedTheta * NR2;    // rfo[NF], pfo[NF]
-  double* SP = RF + 2 * NF;               // populations
+  double* R = sm;                    // u [4][NR2] by TMA, then inv2a f/g, p: [9][NR2]
+  double* RF = R + kStagedTheta * NR2;  // rfo[NF], pfo[NF]
+  double* SP = sm + kThetaSP;        // populations [16][NA] by TMA
   const int x0 = (blockIdx.x % tiles_x) * TX, y0 = (blockIdx.x / tiles_x) * TY;
-  const double* src = state_src(P, s, c->parity);
+  const int parity = c->parity;
+  const double* src = state_src(P, s, parity);
   const double* rows = P.inlet + (long long)s * P.ny * 4;
   const double inv2a = 0.5 / c->a;
   const double gm1 = P.gm1, w = P.w, al = P.alpha;
-  if (threadIdx.x == 0) qn = 0;
-
-  issue_u<2>(P, src, rows, x0, y0, R);
-  cp_async_commit();
-  issue_pops(P, src, rows, x0, y0, inv2a, SP);
-  cp_async_commit();
-  cp_async_wait<1>();
+  if (threadIdx.x == 0) {
+    qn = 0;
+    mbar_init(&bar);
+  }
   __syncthreads();
-  for (int q = threadIdx.x; q < NR2; q += NT) flux_cell(R, NR2, q, inv2a, gm1, true);
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(&bar, kThetaTx);
+    tma_load_4d(R, parity ? &tmu1 : &tmu0, &bar, x0 - 2, y0 - 2, 0, s);
+    tma_load_4d(SP, parity ? &tmp1 : &tmp0, &bar, x0 - 2, y0 - 1, 4, s);
+  }
+  mbar_wait(&bar, 0);
+  if (!(x0 >= 2 && x0 + TX + 2 <= P.nx && y0 >= 2 && y0 + TY + 2 <= P.ny)) {
+    patch_box(P, src, rows, R, RX2, RY2, x0 - 2, y0 - 2, 0, 4, inv2a);
+    patch_box(P, src, rows, SP, AX, AY, x0 - 2, y0 - 1, 4, 16, inv2a);
+    __syncthreads();
+  }
+  double* F = R + 4 * NR2;
+  for (int q = threadIdx.x; q < NR2; q += NT) flux_cell(R, NR2, F, NR2, q, inv2a, gm1, true);
   __syncthreads();
 
   // First-order candidates (compute_candidates, solver.hpp:301-316) on the
   // tile and its 1-ring (the ring corners are never used).
   auto rq = [](int x, int y) { return (y + 2) * RX2 + (x + 2); };
   auto fq = [](int x, int y) { return (y + 1) * FX + (x + 1); };
+  auto M = [&](int q, int k) { return staged_m(R, NR2, F, NR2, q, k, w); };
   auto ufo_at = [&](int x, int y) {
-    const cs a = add(staged_m(R, NR2, rq(x - 1, y), 0, w), staged_m(R, NR2, rq(x + 1, y), 1, w));
-    const cs b = add(staged_m(R, NR2, rq(x, y - 1), 2, w), staged_m(R, NR2, rq(x, y + 1), 3, w));
-    return add(add(a, b), scale(al, staged_u(R, NR2, rq(x, y))));
+    const cs a = add(M(rq(x - 1, y), 0), M(rq(x + 1, y), 1));
+    const cs b = add(M(rq(x, y - 1), 2), M(rq(x, y + 1), 3));
+    return add(add(a, b), scale(al, plane4(R, NR2, rq(x, y))));
   };
   const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
   const cs foC = ufo_at(tx, ty);
@@ -242,7 +226,6 @@ __global__ void __launch_bounds__(tiled::NT, 2) k_theta_tiled(MarchParams P, int
     RF[fq(x, y)] = fo.r;
     RF[NF + fq(x, y)] = pressure(fo, gm1);
   }
-  cp_async_wait<0>();
   __syncthreads();
 
   // Limiter inputs of this thread's cell (face_corrections :321-329,
@@ -253,15 +236,14 @@ __global__ void __launch_bounds__(tiled::NT, 2) k_theta_tiled(MarchParams P, int
   RlmpBounds b;
   bool hard = false;
   if (valid) {
+    auto pop = [&](int k, int x, int y) {
+      return plane4(SP + 4 * k * NA, NA, (y + 1) * AX + (x + 2));
+    };
     const int qc = rq(tx, ty);
-    cf[0] = sub(sub(staged_m(R, NR2, rq(tx - 1, ty), 0, w), spop(SP, 0, tx - 1, ty)),
-                sub(staged_m(R, NR2, qc, 1, w), spop(SP, 1, tx, ty)));
-    cf[1] = sub(sub(staged_m(R, NR2, rq(tx + 1, ty), 1, w), spop(SP, 1, tx + 1, ty)),
-                sub(staged_m(R, NR2, qc, 0, w), spop(SP, 0, tx, ty)));
-    cf[2] = sub(sub(staged_m(R, NR2, rq(tx, ty - 1), 2, w), spop(SP, 2, tx, ty - 1)),
-                sub(staged_m(R, NR2, qc, 3, w), spop(SP, 3, tx, ty)));
-    cf[3] = sub(sub(staged_m(R, NR2, rq(tx, ty + 1), 3, w), spop(SP, 3, tx, ty + 1)),
-                sub(staged_m(R, NR2, qc, 2, w), spop(SP, 2, tx, ty)));
+    cf[0] = sub(sub(M(rq(tx - 1, ty), 0), pop(0, tx - 1, ty)), sub(M(qc, 1), pop(1, tx, ty)));
+    cf[1] = sub(sub(M(rq(tx + 1, ty), 1), pop(1, tx + 1, ty)), sub(M(qc, 0), pop(0, tx, ty)));
+    cf[2] = sub(sub(M(rq(tx, ty - 1), 2), pop(2, tx, ty - 1)), sub(M(qc, 3), pop(3, tx, ty)));
+    cf[3] = sub(sub(M(rq(tx, ty + 1), 3), pop(3, tx, ty + 1)), sub(M(qc, 2), pop(2, tx, ty)));
     RlmpStencil st;
     st.fo = foC;
     const int fpts[5] = {fq(tx, ty), fq(tx - 1, ty), fq(tx + 1, ty), fq(tx, ty - 1), fq(tx, ty + 1)};
@@ -275,7 +257,7 @@ __global__ void __launch_bounds__(tiled::NT, 2) k_theta_tiled(MarchParams P, int
 #pragma unroll
     for (int n = 0; n < 9; ++n) {
       st.rprev[n] = R[rpts[n]];
-      st.pprev[n] = R[12 * NR2 + rpts[n]];
+      st.pprev[n] = F[8 * NR2 + rpts[n]];
     }
     b = rlmp_bounds(st, P.kappa, P.rho_floor_coef, P.p_floor_coef);
     const cs delta = add(add(cf[0], cf[1]), add(cf[2], cf[3]));
@@ -484,29 +466,37 @@ __global__ void __launch_bounds__(256, 2) k_bisect_unc(MarchParams P) {
 
 // ---------------------------------------------------------------------------
 template <int kMode>
-__global__ void __launch_bounds__(tiled::NT, 3) k_advance_tiled(MarchParams P, double const_theta,
-                                                                int tiles_x) {
+__global__ void __launch_bounds__(tiled::NT, 2)
+    k_advance_tiled(MarchParams P, double const_theta, int tiles_x,
+                    const __grid_constant__ CUtensorMap tma0,
+                    const __grid_constant__ CUtensorMap tma1) {
   using namespace tiled;
-  extern __shared__ double sm[];
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) unsigned long long bar;
   const int s = blockIdx.y;
   SampleCtl* c = P.ctl + s;
   if (!c->active) return;
-  double* R = sm;                     // kStagedAdv x NR1
-  double* SP = R + kStagedAdv * NR1;  // populations
+  double* R = sm;          // [20][NA]: u planes 0-3, populations 4-19 (TMA)
+  double* F = sm + kAdvF;  // [8][NA]: inv2a f, inv2a g
   const int x0 = (blockIdx.x % tiles_x) * TX, y0 = (blockIdx.x / tiles_x) * TY;
-  const double* src = state_src(P, s, c->parity);
-  double* dst = state_dst(P, s, c->parity);
+  const int parity = c->parity;
+  const double* src = state_src(P, s, parity);
+  double* dst = state_dst(P, s, parity);
   const double* rows = P.inlet + (long long)s * P.ny * 4;
   const double inv2a = 0.5 / c->a;
   const double gm1 = P.gm1, w = P.w;
-  issue_u<1>(P, src, rows, x0, y0, R);
-  cp_async_commit();
-  issue_pops(P, src, rows, x0, y0, inv2a, SP);
-  cp_async_commit();
-  cp_async_wait<1>();
+  if (threadIdx.x == 0) mbar_init(&bar);
   __syncthreads();
-  for (int q = threadIdx.x; q < NR1; q += NT) flux_cell(R, NR1, q, inv2a, gm1, false);
-  cp_async_wait<0>();
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(&bar, kAdvanceTx);
+    tma_load_4d(R, parity ? &tma1 : &tma0, &bar, x0 - 2, y0 - 1, 0, s);
+  }
+  mbar_wait(&bar, 0);
+  if (!(x0 >= 2 && x0 + TX + 2 <= P.nx && y0 >= 1 && y0 + TY + 1 <= P.ny)) {
+    patch_box(P, src, rows, R, AX, AY, x0 - 2, y0 - 1, 0, 20, inv2a);
+    __syncthreads();
+  }
+  for (int q = threadIdx.x; q < NA; q += NT) flux_cell(R, NA, F, NA, q, inv2a, gm1, false);
   __syncthreads();
 
   const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
@@ -514,28 +504,26 @@ __global__ void __launch_bounds__(tiled::NT, 3) k_advance_tiled(MarchParams P, d
   unsigned long long bits = 0;
   int bad = 0, nonfin = 0;
   if (i < P.nx && j < P.ny) {
-    auto rq = [](int x, int y) { return (y + 1) * RX1 + (x + 1); };
+    auto rq = [](int x, int y) { return (y + 1) * AX + (x + 2); };
+    auto M = [&](int q, int k) { return staged_m(R, NA, F, NA, q, k, w); };
+    auto pop = [&](int k, int q) { return plane4(R + (4 + 4 * k) * NA, NA, q); };
     double tw, te, ts, tn;
     face_thetas<kMode>(P, s, i, j, const_theta, tw, te, ts, tn);
     const long long off = (long long)j * P.pitch + i;
-    const int qc = rq(tx, ty);
-    const cs M0W = staged_m(R, NR1, rq(tx - 1, ty), 0, w);
-    const cs M1E = staged_m(R, NR1, rq(tx + 1, ty), 1, w);
-    const cs M2S = staged_m(R, NR1, rq(tx, ty - 1), 2, w);
-    const cs M3N = staged_m(R, NR1, rq(tx, ty + 1), 3, w);
-    const cs n1 = add(M0W, scale(tw, sub(M0W, spop(SP, 0, tx - 1, ty))));
-    const cs n2 = add(M1E, scale(te, sub(M1E, spop(SP, 1, tx + 1, ty))));
-    const cs n3 = add(M2S, scale(ts, sub(M2S, spop(SP, 2, tx, ty - 1))));
-    const cs n4 = add(M3N, scale(tn, sub(M3N, spop(SP, 3, tx, ty + 1))));
+    const int qc = rq(tx, ty), qw = rq(tx - 1, ty), qe = rq(tx + 1, ty), qs = rq(tx, ty - 1),
+              qn = rq(tx, ty + 1);
+    const cs M0W = M(qw, 0), M1E = M(qe, 1), M2S = M(qs, 2), M3N = M(qn, 3);
+    const cs n1 = add(M0W, scale(tw, sub(M0W, pop(0, qw))));
+    const cs n2 = add(M1E, scale(te, sub(M1E, pop(1, qe))));
+    const cs n3 = add(M2S, scale(ts, sub(M2S, pop(2, qs))));
+    const cs n4 = add(M3N, scale(tn, sub(M3N, pop(3, qn))));
     store_plane4(dst + 4 * P.plane, P.plane, off, n1);
     store_plane4(dst + 8 * P.plane, P.plane, off, n2);
     store_plane4(dst + 12 * P.plane, P.plane, off, n3);
     store_plane4(dst + 16 * P.plane, P.plane, off, n4);
-    cs un = add(add(add(n1, n2), add(n3, n4)), scale(P.alpha, staged_u(R, NR1, qc)));
-    const cs out = add(add(scale(tw, sub(staged_m(R, NR1, qc, 1, w), spop(SP, 1, tx, ty))),
-                           scale(te, sub(staged_m(R, NR1, qc, 0, w), spop(SP, 0, tx, ty)))),
-                       add(scale(ts, sub(staged_m(R, NR1, qc, 3, w), spop(SP, 3, tx, ty))),
-                           scale(tn, sub(staged_m(R, NR1, qc, 2, w), spop(SP, 2, tx, ty)))));
+    cs un = add(add(add(n1, n2), add(n3, n4)), scale(P.alpha, plane4(R, NA, qc)));
+    const cs out = add(add(scale(tw, sub(M(qc, 1), pop(1, qc))), scale(te, sub(M(qc, 0), pop(0, qc)))),
+                       add(scale(ts, sub(M(qc, 3), pop(3, qc))), scale(tn, sub(M(qc, 2), pop(2, qc)))));
     un = sub(un, out);
     store_plane4(dst, P.plane, off, un);
     const double sp = signal_speed(un, P.gamma, gm1, P.conservative);
@@ -577,11 +565,56 @@ static dim3 tiled_grid(const MarchParams& P, int& tiles_x) {
   return dim3(tiles_x * ty, P.S);
 }
 
+// 4-D tensor maps [x = nx, y = ny, plane = 20, sample = S] over both state
+// buffers with the three tile boxes the kernels load.
+int encode_tensor_maps(MarchParams& P) {
+  using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Encode encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        !fn)
+      return set_error(VLBM_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<Encode>(fn);
+  }
+  const cuuint64_t dims[4] = {(cuuint64_t)P.nx, (cuuint64_t)P.ny, (cuuint64_t)kPlanes,
+                              (cuuint64_t)P.S};
+  const cuuint64_t strides[3] = {(cuuint64_t)P.pitch * 8, (cuuint64_t)P.plane * 8,
+                                 (cuuint64_t)P.sample_stride * 8};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  const cuuint32_t box_adv[4] = {tiled::AX, tiled::AY, 20, 1};
+  const cuuint32_t box_thu[4] = {tiled::RX2, tiled::RY2, 4, 1};
+  const cuuint32_t box_thp[4] = {tiled::AX, tiled::AY, 16, 1};
+  for (int b = 0; b < 2; ++b) {
+    void* base = b ? P.buf1 : P.buf0;
+    CUresult r = encode(&P.tm_adv[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, base, dims, strides,
+                        box_adv, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r == CUDA_SUCCESS)
+      r = encode(&P.tm_thu[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, base, dims, strides, box_thu,
+                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r == CUDA_SUCCESS)
+      r = encode(&P.tm_thp[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, base, dims, strides, box_thp,
+                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+      return set_error(VLBM_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  }
+  return VLBM_OK;
+}
+
 cudaError_t launch_theta_tiled(const MarchParams& P, cudaStream_t st) {
   if (cudaError_t e = smem_attrs()) return e;
   int tx;
   const dim3 g = tiled_grid(P, tx);
-  k_theta_tiled<<<g, tiled::NT, tiled::kThetaSmem, st>>>(P, tx);
+  k_theta_tiled<<<g, tiled::NT, tiled::kThetaSmem, st>>>(P, tx, P.tm_thu[0], P.tm_thu[1],
+                                                          P.tm_thp[0], P.tm_thp[1]);
   if (P.hq) {
     k_theta_hard<<<148 * 8, 256, 0, st>>>(P);
     k_bisect_cert<<<148 * 8, 256, 0, st>>>(P);
@@ -597,11 +630,11 @@ cudaError_t launch_advance_tiled(const MarchParams& P, int mode, double const_th
   const dim3 g = tiled_grid(P, tx);
   const size_t sm = tiled::kAdvanceSmem;
   if (mode == 0)
-    k_advance_tiled<0><<<g, tiled::NT, sm, st>>>(P, const_theta, tx);
+    k_advance_tiled<0><<<g, tiled::NT, sm, st>>>(P, const_theta, tx, P.tm_adv[0], P.tm_adv[1]);
   else if (mode == 1)
-    k_advance_tiled<1><<<g, tiled::NT, sm, st>>>(P, const_theta, tx);
+    k_advance_tiled<1><<<g, tiled::NT, sm, st>>>(P, const_theta, tx, P.tm_adv[0], P.tm_adv[1]);
   else
-    k_advance_tiled<2><<<g, tiled::NT, sm, st>>>(P, const_theta, tx);
+    k_advance_tiled<2><<<g, tiled::NT, sm, st>>>(P, const_theta, tx, P.tm_adv[0], P.tm_adv[1]);
   return cudaGetLastError();
 }
 
