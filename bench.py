@@ -227,7 +227,9 @@ def run_reference_arm(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    # default: steps 5..2005 of every sample, i.e. nearly the whole configs[1]
+    # run to t = 0.001 (2207 steps for sample 0), where the limiter's work grows
+    ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--samples", type=int, default=M_PER_GPU)

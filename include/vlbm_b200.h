@@ -196,9 +196,10 @@ int vlbm_batch_stats(vlbm_batch* b, int64_t* launches, double* ms_theta, double*
                      double* ms_sched, int64_t* cell_updates);
 /* Audit of the limiter's certified bisection (test hook): when enabled, every
  * certified bisection step also runs the full 16-check feasible() and counts
- * disagreements.  vlbm_batch_audit fills counters[4]: disagreements (must be
- * 0), bisections entered, bisections certified, vertex-floor failures at the
- * closed-form theta. */
+ * disagreements.  vlbm_batch_audit fills counters[8]: disagreements (must be
+ * 0), bisections entered, fully certified at the closed-form theta,
+ * uncertified, not certifiable, no margin at theta = 0, uncertified vertices
+ * at the start (sum), vertex evaluations in the bisections (sum). */
 int vlbm_batch_set_audit(vlbm_batch* b, int enable);
 int vlbm_batch_audit(vlbm_batch* b, int64_t* counters);
 

@@ -177,9 +177,10 @@ int alloc_batch(const vlbm_grid* g, const vlbm_params* p, int S, int device, vlb
       chk(cudaMalloc(&P.bq_idx, sizeof(long long) * cap), "malloc bq_idx");
       chk(cudaMalloc(&P.cq, sizeof(double) * vlbm_dev::kUncWords * cap), "malloc cq");
       chk(cudaMalloc(&P.cq_idx, sizeof(long long) * cap), "malloc cq_idx");
-      chk(cudaMalloc(&P.hq_n, 4 * sizeof(int)), "malloc hq_n");
+      // counters: [0] hard cells, [2] bq, [3..5] cq bins
+      chk(cudaMalloc(&P.hq_n, 8 * sizeof(int)), "malloc hq_n");
       P.hq_next = P.hq_n + 1;
-      if (rc == VLBM_OK) chk(cudaMemset(P.hq_n, 0, 4 * sizeof(int)), "memset hq_n");
+      if (rc == VLBM_OK) chk(cudaMemset(P.hq_n, 0, 8 * sizeof(int)), "memset hq_n");
     }
   }
   if (rc == VLBM_OK) rc = vlbm_impl::encode_tensor_maps(P);
@@ -526,8 +527,8 @@ int vlbm_batch_set_audit(vlbm_batch* b, int enable) {
   if (!b) return set_error(VLBM_E_INVALID, "null batch");
   CU(cudaSetDevice(b->device));
   if (enable && !b->P.audit) {
-    CU(cudaMalloc(&b->P.audit, 4 * sizeof(int)));
-    CU(cudaMemset(b->P.audit, 0, 4 * sizeof(int)));
+    CU(cudaMalloc(&b->P.audit, 8 * sizeof(int)));
+    CU(cudaMemset(b->P.audit, 0, 8 * sizeof(int)));
   } else if (!enable && b->P.audit) {
     CU(cudaFree(b->P.audit));
     b->P.audit = nullptr;
@@ -537,12 +538,12 @@ int vlbm_batch_set_audit(vlbm_batch* b, int enable) {
 
 int vlbm_batch_audit(vlbm_batch* b, int64_t* counters) {
   if (!b || !counters) return set_error(VLBM_E_INVALID, "null argument");
-  int h[4] = {0, 0, 0, 0};
+  int h[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   if (b->P.audit) {
     CU(cudaMemcpyAsync(h, b->P.audit, sizeof(h), cudaMemcpyDeviceToHost, b->stream));
     CU(cudaStreamSynchronize(b->stream));
   }
-  for (int k = 0; k < 4; ++k) counters[k] = h[k];
+  for (int k = 0; k < 8; ++k) counters[k] = h[k];
   return VLBM_OK;
 }
 

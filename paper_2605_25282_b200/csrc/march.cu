@@ -146,7 +146,8 @@ __global__ void k_sched(MarchParams P, double target, double fixed_dt) {
   __syncthreads();
   if (threadIdx.x == 0) {
     *P.n_active = s_count;
-    if (P.hq_n) P.hq_n[0] = P.hq_n[1] = P.hq_n[2] = P.hq_n[3] = 0;  // empty the limiter queues
+    if (P.hq_n)  // empty the limiter queues
+      for (int k = 0; k < 8; ++k) P.hq_n[k] = 0;
   }
 }
 

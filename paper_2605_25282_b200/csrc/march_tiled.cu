@@ -336,14 +336,22 @@ __device__ __forceinline__ void load_hard_entry(const MarchParams& P, int slot, 
 
 constexpr long long kIdxMask = (1ll << 40) - 1;
 
+// Uncertified bisections are binned by their number of uncertified vertices
+// (1, 2, >= 3) into thirds of cq, so lanes of a warp run similar vertex loops.
+__device__ __forceinline__ int unc_class(unsigned unc) {
+  const int n = __popc(unc);
+  return n <= 1 ? 0 : (n == 2 ? 1 : 2);
+}
+
 __global__ void __launch_bounds__(256, 2) k_theta_hard(MarchParams P) {
-  __shared__ int nb, nc, baseb, basec;
+  __shared__ int nb, nc[3], baseb, basec[3];
   const int n = min(P.hq_n[0], P.hq_cap);
   const long long cap = P.hq_cap;
   const double gm1 = P.gm1;
   for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
     const int slot = base + threadIdx.x;
     int cls = 0;  // 0: finished here, 1: -> bq, 2: -> cq
+    int ccls = 0;  // cq bin
     long long idx = -1;
     cs fo, cf[4], delta;
     RlmpBounds b;
@@ -361,6 +369,7 @@ __global__ void __launch_bounds__(256, 2) k_theta_hard(MarchParams P) {
           P.theta[idx] = h.result;
         } else {
           cls = (h.unc || P.audit) ? 2 : 1;
+          ccls = unc_class(h.unc);
           if (P.audit) {
             atomicAdd(P.audit + 1, 1);
             atomicAdd(P.audit + (h.unc ? 3 : 2), 1);
@@ -368,17 +377,18 @@ __global__ void __launch_bounds__(256, 2) k_theta_hard(MarchParams P) {
         }
       }
     }
-    if (threadIdx.x == 0) nb = nc = 0;
+    if (threadIdx.x == 0) nb = nc[0] = nc[1] = nc[2] = 0;
     __syncthreads();
     int my = 0;
     if (cls == 1) my = atomicAdd(&nb, 1);
-    if (cls == 2) my = atomicAdd(&nc, 1);
+    if (cls == 2) my = atomicAdd(&nc[ccls], 1);
     __syncthreads();
     if (threadIdx.x == 0) {
       baseb = nb ? atomicAdd(P.hq_n + 2, nb) : 0;
-      basec = nc ? atomicAdd(P.hq_n + 3, nc) : 0;
+      for (int k = 0; k < 3; ++k) basec[k] = nc[k] ? atomicAdd(P.hq_n + 3 + k, nc[k]) : 0;
     }
     __syncthreads();
+    const int third = P.hq_cap / 3;
     if (cls == 1) {
       const int s = baseb + my;
       if (baseb + nb <= P.hq_cap) {
@@ -393,8 +403,8 @@ __global__ void __launch_bounds__(256, 2) k_theta_hard(MarchParams P) {
         P.theta[idx] = bisect_certified(fo, delta, b, h.thc, gm1);
       }
     } else if (cls == 2) {
-      const int s = basec + my;
-      if (basec + nc <= P.hq_cap) {
+      const int s = ccls * third + basec[ccls] + my;
+      if (basec[ccls] + nc[ccls] <= third) {
         double* q = P.cq + s;
         q[0] = fo.r, q[cap] = fo.mx, q[2 * cap] = fo.my, q[3 * cap] = fo.e;
 #pragma unroll
@@ -408,9 +418,9 @@ __global__ void __launch_bounds__(256, 2) k_theta_hard(MarchParams P) {
         q[24 * cap] = h.thc, q[25 * cap] = h.p0;
         q[26 * cap] = h.certifiable ? h.err : -1.0;
         q[27 * cap] = h.er;
-        P.cq_idx[s] = idx | ((long long)h.unc << 40);
+        P.cq_idx[s] = idx | ((long long)h.mhi << 40) | ((long long)h.lo_all << 56);
       } else {
-        if (s < P.hq_cap) P.cq_idx[s] = -1;
+        if (basec[ccls] + my < third) P.cq_idx[s] = -1;
         P.theta[idx] = bisect_uncertified(fo, cf, delta, b, h, gm1, P.audit);
       }
     }
@@ -434,10 +444,13 @@ __global__ void __launch_bounds__(256) k_bisect_cert(MarchParams P) {
   }
 }
 
+// blockIdx.y = cq bin; bins run concurrently.
 __global__ void __launch_bounds__(256, 2) k_bisect_unc(MarchParams P) {
-  const int n = min(P.hq_n[3], P.hq_cap);
+  const int third = P.hq_cap / 3;
+  const int n = min(P.hq_n[3 + blockIdx.y], third);
   const long long cap = P.hq_cap;
-  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gridDim.x * blockDim.x) {
+  for (int s0 = blockIdx.x * blockDim.x + threadIdx.x; s0 < n; s0 += gridDim.x * blockDim.x) {
+    const int s = (int)blockIdx.y * third + s0;
     const long long packed = P.cq_idx[s];
     if (packed < 0) continue;
     const double* q = P.cq + s;
@@ -458,7 +471,9 @@ __global__ void __launch_bounds__(256, 2) k_bisect_unc(MarchParams P) {
     h.err = q[26 * cap];
     h.certifiable = h.err >= 0.0;
     h.er = q[27 * cap];
-    h.unc = (unsigned)(packed >> 40);
+    h.mhi = (unsigned)(packed >> 40) & kAllVertices;
+    h.lo_all = ((packed >> 56) & 1) != 0;
+    h.unc = kAllVertices & ~((h.lo_all ? kAllVertices : 0u) & h.mhi);
     const cs delta = add(add(cf[0], cf[1]), add(cf[2], cf[3]));
     P.theta[packed & kIdxMask] = bisect_uncertified(fo, cf, delta, b, h, P.gm1, P.audit);
   }
@@ -618,7 +633,7 @@ cudaError_t launch_theta_tiled(const MarchParams& P, cudaStream_t st) {
   if (P.hq) {
     k_theta_hard<<<148 * 8, 256, 0, st>>>(P);
     k_bisect_cert<<<148 * 8, 256, 0, st>>>(P);
-    k_bisect_unc<<<148 * 8, 256, 0, st>>>(P);
+    k_bisect_unc<<<dim3(148 * 3, 3), 256, 0, st>>>(P);
   }
   return cudaGetLastError();
 }

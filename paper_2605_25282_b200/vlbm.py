@@ -381,9 +381,11 @@ class BatchSimulation:
         _check(lib().vlbm_batch_set_audit(self._h, int(on)))
 
     def audit_counters(self) -> dict:
-        n = (I64 * 4)()
+        n = (I64 * 8)()
         _check(lib().vlbm_batch_audit(self._h, n))
-        return dict(mismatches=n[0], bisections=n[1], certified=n[2], vertex_fail_at_thc=n[3])
+        return dict(mismatches=n[0], bisections=n[1], certified_at_thc=n[2], uncertified=n[3],
+                    not_certifiable=n[4], no_margin_at_0=n[5], unc_vertices_start=n[6],
+                    vertex_evals=n[7])
 
     def audit_mismatches(self) -> int:
         return self.audit_counters()["mismatches"]
