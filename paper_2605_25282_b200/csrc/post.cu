@@ -187,70 +187,104 @@ __device__ __forceinline__ void warp_bitonic_sort(unsigned long long (&v)[R], in
 // Per-cell term: sum_m |a_(m) - b_(m)| over sorted ranks, sequential in m,
 // divided by M (metrics.hpp:118-122).  Loader functors return sample m's
 // value of the warp's cell.
-template <int R, class LA, class LB>
-__device__ __forceinline__ double w1_cell(int M, int lane, LA la, LB lb) {
-  unsigned long long ka[R], kb[R];
+// ca / cb: the cell's M values of each ensemble in shared memory (ca is
+// overwritten).  One ensemble is sorted at a time (R keys per lane in
+// registers); the sorted first column is parked in ca at slot (r, lane) so the
+// second sort has the registers to itself.  Rank e = lane*R + r; the chain
+// visits lanes in order, each adding its R terms, so the sum is strictly
+// sequential in rank as in the reference.
+template <int R>
+__device__ __forceinline__ double w1_cell(int M, int lane, double* ca, const double* cb) {
+  unsigned long long k[R];
+#pragma unroll 1
+  for (int pass = 0; pass < 2; ++pass) {
+    const double* col = pass ? cb : ca;
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int m = r * 32 + lane;  // load slot: coalesced order; sorting is order-free
-    ka[r] = m < M ? dkey(la(m)) : ~0ull;
-    kb[r] = m < M ? dkey(lb(m)) : ~0ull;
+    for (int r = 0; r < R; ++r) {
+      const int m = r * 32 + lane;  // load slot order is free: sorting is order-free
+      k[r] = m < M ? dkey(col[m]) : ~0ull;
+    }
+    warp_bitonic_sort<R>(k, lane);
+    if (pass == 0) {
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < R; ++r) ca[r * 32 + lane] = dval(k[r]);
+      __syncwarp();
+    }
   }
-  warp_bitonic_sort<R>(ka, lane);
-  warp_bitonic_sort<R>(kb, lane);
-  // Ranks lane*R .. lane*R+R-1 live in this lane: the chain visits lanes in
-  // order, each adding its R terms, so the sum is strictly sequential in m.
+  // terms |a_(e) - b_(e)| in parallel, in place in ca (padded ranks
+  // contribute nothing); then only the dependent adds run lane after lane
+#pragma unroll
+  for (int r = 0; r < R; ++r) ca[r * 32 + lane] = fabs(ca[r * 32 + lane] - dval(k[r]));
+  __syncwarp();
+  const int valid = M - lane * R;  // ranks of this lane that exist
   double cell = 0.0;
+#pragma unroll 1
   for (int L = 0; L < 32; ++L) {
     if (lane == L) {
 #pragma unroll
       for (int r = 0; r < R; ++r)
-        if (L * R + r < M) cell += fabs(dval(ka[r]) - dval(kb[r]));
+        if (r < valid) cell += ca[r * 32 + L];
     }
     cell = __shfl_sync(kFull, cell, L);
   }
   return cell / static_cast<double>(M);
 }
 
-// Sample-major planes: value(m, c) = a[m * a_stride + c].
-template <int R>
-__global__ void __launch_bounds__(256) k_w1_planes(int M, long long n, const double* a,
-                                                   long long as, const double* b, long long bs,
-                                                   double* terms) {
-  const int lane = threadIdx.x & 31;
-  const long long c = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (c >= n) return;
-  const double t = w1_cell<R>(
-      M, lane, [&](int m) { return a[(long long)m * as + c]; },
-      [&](int m) { return b[(long long)m * bs + c]; });
-  if (lane == 0) terms[c] = t;
-}
+// A CTA of kW1Cells warps owns kW1Cells consecutive cells, one warp per cell.
+// The M values of both ensembles for its cells are staged into shared memory
+// [cell][m] with sector-efficient loads, then each warp reduces its cell.
+//   kKind 0: sample-major planes, value(m, c) = a[m*as + c], b[m*bs + c]
+//   kKind 1: coarse planes vs the restriction of fine planes (b = fine,
+//            bs = fine sample stride; 32-byte coarse and two 64-byte fine
+//            segments per sample, every fetched sector fully used)
+//   kKind 2: cell-major columns after the sample->cell re-shard, a[c*M + m]
+constexpr int kW1Cells = 4;
 
-// Coarse planes vs restricted fine planes (restriction fused).
-template <int R>
-__global__ void __launch_bounds__(256) k_w1_restrict(int M, int nxc, int nyc, const double* a,
-                                                     long long as, const double* f,
-                                                     long long fs, double* terms) {
-  const int lane = threadIdx.x & 31;
-  const long long n = (long long)nxc * nyc;
-  const long long c = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+template <int R, int kKind>
+__global__ void __launch_bounds__(32 * kW1Cells, 4) k_w1_tile(int M, long long n, int nxc,
+                                                           const double* a, long long as,
+                                                           const double* b, long long bs,
+                                                           double* terms) {
+  extern __shared__ double smw[];
+  constexpr int LD = 32 * R + 1;  // padded column stride (conflict-free transposed stores)
+  double* sa = smw;
+  double* sb = smw + kW1Cells * LD;
+  const long long c0 = (long long)blockIdx.x * kW1Cells;
+#pragma unroll 4
+  for (int e = threadIdx.x; e < M * kW1Cells; e += blockDim.x) {
+    int m, cl;
+    if (kKind == 2) {
+      cl = e / M;
+      m = e - cl * M;
+    } else {
+      m = e / kW1Cells;
+      cl = e - m * kW1Cells;
+    }
+    const long long c = c0 + cl;
+    double va = 0.0, vb = 0.0;
+    if (c < n) {
+      if (kKind == 2) {
+        va = a[c * M + m];
+        vb = b[c * M + m];
+      } else {
+        va = a[(long long)m * as + c];
+        if (kKind == 1) {
+          const int j = (int)(c / nxc), i = (int)(c - (long long)j * nxc);
+          vb = restrict_at(b + (long long)m * bs, 2 * nxc, i, j);
+        } else {
+          vb = b[(long long)m * bs + c];
+        }
+      }
+    }
+    sa[cl * LD + m] = va;
+    sb[cl * LD + m] = vb;
+  }
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long c = c0 + w;
   if (c >= n) return;
-  const int j = (int)(c / nxc), i = (int)(c - (long long)j * nxc);
-  const double t = w1_cell<R>(
-      M, lane, [&](int m) { return a[(long long)m * as + c]; },
-      [&](int m) { return restrict_at(f + (long long)m * fs, 2 * nxc, i, j); });
-  if (lane == 0) terms[c] = t;
-}
-
-// Cell-major columns (after the sample->cell re-shard): value(m, c) = a[c*M + m].
-template <int R>
-__global__ void __launch_bounds__(256) k_w1_cells(int M, long long n, const double* a,
-                                                  const double* b, double* terms) {
-  const int lane = threadIdx.x & 31;
-  const long long c = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (c >= n) return;
-  const double t = w1_cell<R>(
-      M, lane, [&](int m) { return a[c * M + m]; }, [&](int m) { return b[c * M + m]; });
+  const double t = w1_cell<R>(M, lane, sa + w * LD, sb + w * LD);
   if (lane == 0) terms[c] = t;
 }
 
@@ -349,45 +383,45 @@ cudaError_t launch_strong_partials_var(int M, int nxc, int nyc, const double* co
   return cudaGetLastError();
 }
 
-#define W1_DISPATCH(KERNEL, M, grid, st, ...)                                   \
-  do {                                                                          \
-    if ((M) <= 32)                                                              \
-      KERNEL<1><<<grid, 256, 0, st>>>(__VA_ARGS__);                             \
-    else if ((M) <= 64)                                                         \
-      KERNEL<2><<<grid, 256, 0, st>>>(__VA_ARGS__);                             \
-    else if ((M) <= 128)                                                        \
-      KERNEL<4><<<grid, 256, 0, st>>>(__VA_ARGS__);                             \
-    else if ((M) <= 256)                                                        \
-      KERNEL<8><<<grid, 256, 0, st>>>(__VA_ARGS__);                             \
-    else if ((M) <= 512)                                                        \
-      KERNEL<16><<<grid, 256, 0, st>>>(__VA_ARGS__);                            \
-    else                                                                        \
-      KERNEL<32><<<grid, 256, 0, st>>>(__VA_ARGS__);                            \
-  } while (0)
+// W1 launch for M <= 1024: R = keys per lane (next power of two of M/32).
+template <int kKind>
+static cudaError_t launch_w1(int M, long long n, int nxc, const double* a, long long as,
+                             const double* b, long long bs, double* terms, cudaStream_t st) {
+  if (M < 1 || M > 1024) return cudaErrorInvalidValue;
+  const int grid = (int)((n + kW1Cells - 1) / kW1Cells);
+  auto go = [&](auto kernel, int R) {
+    const size_t smem = sizeof(double) * 2 * kW1Cells * (32 * R + 1);
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kernel<<<grid, 32 * kW1Cells, smem, st>>>(M, n, nxc, a, as, b, bs, terms);
+  };
+  if (M <= 32)
+    go(k_w1_tile<1, kKind>, 1);
+  else if (M <= 64)
+    go(k_w1_tile<2, kKind>, 2);
+  else if (M <= 128)
+    go(k_w1_tile<4, kKind>, 4);
+  else if (M <= 256)
+    go(k_w1_tile<8, kKind>, 8);
+  else if (M <= 512)
+    go(k_w1_tile<16, kKind>, 16);
+  else
+    go(k_w1_tile<32, kKind>, 32);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_w1_planes(int M, int64_t n, const double* a, int64_t as, const double* b,
                              int64_t bs, double* terms, cudaStream_t st) {
-  if (M < 1 || M > 1024) return cudaErrorInvalidValue;
-  const int grid = (int)((n + 7) / 8);
-  W1_DISPATCH(k_w1_planes, M, grid, st, M, n, a, as, b, bs, terms);
-  return cudaGetLastError();
+  return launch_w1<0>(M, n, 0, a, as, b, bs, terms, st);
 }
 
 cudaError_t launch_w1_restrict(int M, int nxc, int nyc, const double* a, int64_t as,
                                const double* f, int64_t fs, double* terms, cudaStream_t st) {
-  if (M < 1 || M > 1024) return cudaErrorInvalidValue;
-  const long long n = (long long)nxc * nyc;
-  const int grid = (int)((n + 7) / 8);
-  W1_DISPATCH(k_w1_restrict, M, grid, st, M, nxc, nyc, a, as, f, fs, terms);
-  return cudaGetLastError();
+  return launch_w1<1>(M, (long long)nxc * nyc, nxc, a, as, f, fs, terms, st);
 }
 
 cudaError_t launch_w1_cells(int M, int64_t n, const double* a, const double* b, double* terms,
                             cudaStream_t st) {
-  if (M < 1 || M > 1024) return cudaErrorInvalidValue;
-  const int grid = (int)((n + 7) / 8);
-  W1_DISPATCH(k_w1_cells, M, grid, st, M, n, a, b, terms);
-  return cudaGetLastError();
+  return launch_w1<2>(M, n, 0, a, 0, b, 0, terms, st);
 }
 
 cudaError_t launch_ordered_mean(int64_t n, const double* terms, double* result, cudaStream_t st) {
