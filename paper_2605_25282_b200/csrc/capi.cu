@@ -7,7 +7,9 @@
 // VLBM_E_CUDA.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -57,7 +59,16 @@ struct vlbm_batch {
   double ms_theta = 0, ms_advance = 0, ms_sched = 0;
   std::vector<cudaEvent_t> ev;  // pool of events, pairs per timed launch
   std::vector<int> ev_kind;     // 0 sched, 1 theta, 2 advance
+  std::vector<cudaStream_t> ev_stream;
   int ev_used = 0;
+  // sample groups (march views), see alloc_batch
+  int G = 1;
+  std::vector<MarchParams> Pg;
+  std::vector<cudaStream_t> sg;  // sg[0] == stream
+  std::vector<int> g0;           // first sample of each group
+  int* d_active_g = nullptr;
+  int* h_active_g = nullptr;     // pinned
+  cudaEvent_t ev_fork = nullptr;
 };
 
 namespace {
@@ -84,13 +95,20 @@ void free_batch(vlbm_batch* b) {
   cudaFree(b->P.ctl);
   cudaFree(b->P.n_active);
   cudaFree(b->d_a0);
-  cudaFree(b->P.hq);
-  cudaFree(b->P.hq_idx);
-  cudaFree(b->P.hq_n);
-  cudaFree(b->P.bq);
-  cudaFree(b->P.bq_idx);
-  cudaFree(b->P.cq);
-  cudaFree(b->P.cq_idx);
+  for (size_t g = 0; g < b->Pg.size(); ++g) {
+    MarchParams& Q = b->Pg[g];
+    cudaFree(Q.hq);
+    cudaFree(Q.hq_idx);
+    cudaFree(Q.hq_n);
+    cudaFree(Q.bq);
+    cudaFree(Q.bq_idx);
+    cudaFree(Q.cq);
+    cudaFree(Q.cq_idx);
+    if (g > 0 && b->sg[g]) cudaStreamDestroy(b->sg[g]);
+  }
+  cudaFree(b->d_active_g);
+  if (b->h_active_g) cudaFreeHost(b->h_active_g);
+  if (b->ev_fork) cudaEventDestroy(b->ev_fork);
   cudaFree(b->d_face_tx);
   cudaFree(b->d_face_ty);
   cudaFree(b->P.audit);
@@ -159,29 +177,57 @@ int alloc_batch(const vlbm_grid* g, const vlbm_params* p, int S, int device, vlb
   chk(cudaMalloc(&P.n_active, sizeof(int)), "malloc n_active");
   chk(cudaMalloc(&b->d_a0, sizeof(double) * S), "malloc a0");
   chk(cudaMallocHost(&b->h_active, sizeof(int)), "malloc host");
-  // Limiter hard-cell queue: up to every cell of the batch, capped by memory
+  // Sample groups: the march runs G views of the batch (disjoint sample
+  // ranges: offset pointers, own control slice, limiter queues, tensor maps,
+  // counter and stream), so one group's HBM-bound advance overlaps another
+  // group's FP64-bound limiter.  VLBM_GROUPS overrides the default.
+  int G = S >= 8 ? 2 : 1;
+  if (const char* e = getenv("VLBM_GROUPS")) G = std::max(1, std::min(S, atoi(e)));
+  b->G = G;
+  chk(cudaMalloc(&b->d_active_g, sizeof(int) * G), "malloc active_g");
+  chk(cudaMallocHost(&b->h_active_g, sizeof(int) * G), "malloc host active_g");
+  chk(cudaEventCreateWithFlags(&b->ev_fork, cudaEventDisableTiming), "event");
+  // Limiter queues per group: up to every cell of the group, capped by memory
   // (overflowing CTAs finish their hard cells in place).
-  if (p->limiter == VLBM_LIMITER_RLMP && rc == VLBM_OK) {
-    const size_t entry =
-        sizeof(double) * (vlbm_dev::kHardWords + vlbm_dev::kBisWords + vlbm_dev::kUncWords) +
-        3 * sizeof(long long);
-    size_t cap = (size_t)S * P.nx * P.ny;
-    size_t avail = free_b > need + (size_t)(2ull << 30) ? free_b - need - (size_t)(2ull << 30) : 0;
-    if (cap * entry > avail / 2) cap = avail / 2 / entry;
-    if (cap > (size_t)INT_MAX / 2) cap = (size_t)INT_MAX / 2;
-    if (cap >= 1024) {
-      P.hq_cap = (int)cap;
-      chk(cudaMalloc(&P.hq, sizeof(double) * vlbm_dev::kHardWords * cap), "malloc hq");
-      chk(cudaMalloc(&P.hq_idx, sizeof(long long) * cap), "malloc hq_idx");
-      chk(cudaMalloc(&P.bq, sizeof(double) * vlbm_dev::kBisWords * cap), "malloc bq");
-      chk(cudaMalloc(&P.bq_idx, sizeof(long long) * cap), "malloc bq_idx");
-      chk(cudaMalloc(&P.cq, sizeof(double) * vlbm_dev::kUncWords * cap), "malloc cq");
-      chk(cudaMalloc(&P.cq_idx, sizeof(long long) * cap), "malloc cq_idx");
-      // counters: [0] hard cells, [2] bq, [3..5] cq bins
-      chk(cudaMalloc(&P.hq_n, 8 * sizeof(int)), "malloc hq_n");
-      P.hq_next = P.hq_n + 1;
-      if (rc == VLBM_OK) chk(cudaMemset(P.hq_n, 0, 8 * sizeof(int)), "memset hq_n");
+  const size_t entry =
+      sizeof(double) * (vlbm_dev::kHardWords + vlbm_dev::kBisWords + vlbm_dev::kUncWords) +
+      3 * sizeof(long long);
+  const size_t avail =
+      free_b > need + (size_t)(2ull << 30) ? free_b - need - (size_t)(2ull << 30) : 0;
+  for (int g = 0; g < G && rc == VLBM_OK; ++g) {
+    const int s0 = (int)((long long)S * g / G), s1 = (int)((long long)S * (g + 1) / G);
+    MarchParams Q = P;
+    Q.S = s1 - s0;
+    Q.ctl = P.ctl + s0;
+    Q.buf0 = P.buf0 + (size_t)s0 * P.sample_stride;
+    Q.buf1 = P.buf1 + (size_t)s0 * P.sample_stride;
+    Q.theta = P.theta + (size_t)s0 * P.plane;
+    Q.inlet = P.inlet + (size_t)s0 * P.ny * 4;
+    Q.n_active = b->d_active_g + g;
+    cudaStream_t sg = b->stream;
+    if (g > 0) chk(cudaStreamCreateWithFlags(&sg, cudaStreamNonBlocking), "stream g");
+    if (p->limiter == VLBM_LIMITER_RLMP) {
+      size_t cap = (size_t)Q.S * P.nx * P.ny;
+      if (cap * entry > avail / 2 / G) cap = avail / 2 / G / entry;
+      if (cap > (size_t)INT_MAX / 2) cap = (size_t)INT_MAX / 2;
+      if (cap >= 1024) {
+        Q.hq_cap = (int)cap;
+        chk(cudaMalloc(&Q.hq, sizeof(double) * vlbm_dev::kHardWords * cap), "malloc hq");
+        chk(cudaMalloc(&Q.hq_idx, sizeof(long long) * cap), "malloc hq_idx");
+        chk(cudaMalloc(&Q.bq, sizeof(double) * vlbm_dev::kBisWords * cap), "malloc bq");
+        chk(cudaMalloc(&Q.bq_idx, sizeof(long long) * cap), "malloc bq_idx");
+        chk(cudaMalloc(&Q.cq, sizeof(double) * vlbm_dev::kUncWords * cap), "malloc cq");
+        chk(cudaMalloc(&Q.cq_idx, sizeof(long long) * cap), "malloc cq_idx");
+        // counters: [0] hard cells, [2] bq, [3..5] cq bins
+        chk(cudaMalloc(&Q.hq_n, 8 * sizeof(int)), "malloc hq_n");
+        Q.hq_next = Q.hq_n + 1;
+        if (rc == VLBM_OK) chk(cudaMemset(Q.hq_n, 0, 8 * sizeof(int)), "memset hq_n");
+      }
     }
+    if (rc == VLBM_OK) rc = vlbm_impl::encode_tensor_maps(Q);
+    b->Pg.push_back(Q);
+    b->sg.push_back(sg);
+    b->g0.push_back(s0);
   }
   if (rc == VLBM_OK) rc = vlbm_impl::encode_tensor_maps(P);
   if (rc == VLBM_OK) {
@@ -228,20 +274,27 @@ int finish_create(vlbm_batch* b) {
   return VLBM_OK;
 }
 
-void record(vlbm_batch* b, int kind) {
+// Kernel timing (CUDA events around each launch on its own stream).  With
+// several sample groups the per-kind sums add the groups' (overlapping)
+// kernel times.
+void record(vlbm_batch* b, int kind, cudaStream_t st) {
   if (!b->timing) return;
   while ((int)b->ev.size() < 2 * (b->ev_used + 1)) {
     cudaEvent_t e;
     cudaEventCreate(&e);
     b->ev.push_back(e);
   }
-  if ((int)b->ev_kind.size() < b->ev_used + 1) b->ev_kind.resize(b->ev_used + 1);
+  if ((int)b->ev_kind.size() < b->ev_used + 1) {
+    b->ev_kind.resize(b->ev_used + 1);
+    b->ev_stream.resize(b->ev_used + 1);
+  }
   b->ev_kind[b->ev_used] = kind;
-  cudaEventRecord(b->ev[2 * b->ev_used], b->stream);
+  b->ev_stream[b->ev_used] = st;
+  cudaEventRecord(b->ev[2 * b->ev_used], st);
 }
 void record_end(vlbm_batch* b) {
   if (!b->timing) return;
-  cudaEventRecord(b->ev[2 * b->ev_used + 1], b->stream);
+  cudaEventRecord(b->ev[2 * b->ev_used + 1], b->ev_stream[b->ev_used]);
   ++b->ev_used;
 }
 void harvest(vlbm_batch* b) {
@@ -264,29 +317,40 @@ void harvest(vlbm_batch* b) {
 // means every sample has reached the target (or diverged / used its budget)
 // and every step taken is finalised.
 int march_loop(vlbm_batch* b, double target, double fixed_dt, int mode, int chunk) {
-  const MarchParams& P = b->P;
   const bool rlmp = b->p.limiter == VLBM_LIMITER_RLMP && mode == 0;
   const int adv_mode = mode == 2 ? 2 : (rlmp ? 0 : 1);
   const double const_theta = b->p.limiter == VLBM_LIMITER_SECOND_ORDER ? 1.0 : 0.0;
+  const int G = b->G;
   for (;;) {
+    // fork: the group streams start after everything queued on the main stream
+    CU(cudaEventRecord(b->ev_fork, b->stream));
+    for (int g = 1; g < G; ++g) CU(cudaStreamWaitEvent(b->sg[g], b->ev_fork, 0));
     for (int it = 0; it < chunk; ++it) {
-      record(b, 0);
-      CU(vlbm_impl::launch_sched(P, target, fixed_dt, b->stream));
-      record_end(b);
-      if (rlmp) {
-        record(b, 1);
-        CU(vlbm_impl::launch_theta(P, b->stream));
+      for (int g = 0; g < G; ++g) {  // groups interleaved: their kernels overlap
+        const MarchParams& Q = b->Pg[g];
+        cudaStream_t st = b->sg[g];
+        record(b, 0, st);
+        CU(vlbm_impl::launch_sched(Q, target, fixed_dt, st));
         record_end(b);
+        if (rlmp) {
+          record(b, 1, st);
+          CU(vlbm_impl::launch_theta(Q, st));
+          record_end(b);
+        }
+        record(b, 2, st);
+        CU(vlbm_impl::launch_advance(Q, adv_mode, const_theta, st));
+        record_end(b);
+        b->launches += rlmp ? (Q.hq ? 6 : 3) : 2;
       }
-      record(b, 2);
-      CU(vlbm_impl::launch_advance(P, adv_mode, const_theta, b->stream));
-      record_end(b);
-      b->launches += rlmp ? (P.hq ? 6 : 3) : 2;
     }
-    CU(cudaMemcpyAsync(b->h_active, P.n_active, sizeof(int), cudaMemcpyDeviceToHost, b->stream));
-    CU(cudaStreamSynchronize(b->stream));
+    for (int g = 0; g < G; ++g)
+      CU(cudaMemcpyAsync(b->h_active_g + g, b->Pg[g].n_active, sizeof(int),
+                         cudaMemcpyDeviceToHost, b->sg[g]));
+    for (int g = 0; g < G; ++g) CU(cudaStreamSynchronize(b->sg[g]));
     if (b->timing) harvest(b);
-    if (*b->h_active == 0) return VLBM_OK;
+    int active = 0;
+    for (int g = 0; g < G; ++g) active += b->h_active_g[g];
+    if (active == 0) return VLBM_OK;
     if (mode == 2) chunk = 1;
   }
 }
@@ -429,6 +493,10 @@ int vlbm_batch_step_with_blending(vlbm_batch* b, double dt, const double* theta_
                      b->stream));
   b->P.face_tx = b->d_face_tx;
   b->P.face_ty = b->d_face_ty;
+  for (int g = 0; g < b->G; ++g) {
+    b->Pg[g].face_tx = b->d_face_tx + (size_t)b->g0[g] * b->g.ny * (b->g.nx + 1);
+    b->Pg[g].face_ty = b->d_face_ty + (size_t)b->g0[g] * (b->g.ny + 1) * b->g.nx;
+  }
   CU(vlbm_impl::launch_set_budget(b->P, 1, b->stream));
   ++b->launches;
   const double inf = std::numeric_limits<double>::infinity();
@@ -533,6 +601,7 @@ int vlbm_batch_set_audit(vlbm_batch* b, int enable) {
     CU(cudaFree(b->P.audit));
     b->P.audit = nullptr;
   }
+  for (auto& Q : b->Pg) Q.audit = b->P.audit;
   return VLBM_OK;
 }
 

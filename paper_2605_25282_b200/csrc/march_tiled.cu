@@ -42,10 +42,11 @@ constexpr int kStagedTheta = 13;  // u(4) [TMA], inv2a*f(4), inv2a*g(4), p
 constexpr int kThetaSP = ((kStagedTheta * NR2 + 2 * NF) + 15) / 16 * 16;
 constexpr size_t kThetaSmem = sizeof(double) * (kThetaSP + 16 * NA);
 constexpr unsigned kThetaTx = sizeof(double) * (4 * NR2 + 16 * NA);
-// advance smem: R [20][NA] (TMA: u + pops) | F [8][NA] (inv2a f, inv2a g)
-constexpr int kAdvF = 20 * NA;
+// advance smem: R [4][NA] (TMA: u) | F [8][NA] (inv2a f, inv2a g); the
+// populations are read from global memory by their pulling thread.
+constexpr int kAdvF = 4 * NA;
 constexpr size_t kAdvanceSmem = sizeof(double) * (kAdvF + 8 * NA);
-constexpr unsigned kAdvanceTx = sizeof(double) * 20 * NA;
+constexpr unsigned kAdvanceTx = sizeof(double) * 4 * NA;
 }  // namespace tiled
 
 // ---- TMA + mbarrier (PTX) -----------------------------------------------------
@@ -481,7 +482,7 @@ __global__ void __launch_bounds__(256, 2) k_bisect_unc(MarchParams P) {
 
 // ---------------------------------------------------------------------------
 template <int kMode>
-__global__ void __launch_bounds__(tiled::NT, 2)
+__global__ void __launch_bounds__(tiled::NT, 3)
     k_advance_tiled(MarchParams P, double const_theta, int tiles_x,
                     const __grid_constant__ CUtensorMap tma0,
                     const __grid_constant__ CUtensorMap tma1) {
@@ -491,7 +492,7 @@ __global__ void __launch_bounds__(tiled::NT, 2)
   const int s = blockIdx.y;
   SampleCtl* c = P.ctl + s;
   if (!c->active) return;
-  double* R = sm;          // [20][NA]: u planes 0-3, populations 4-19 (TMA)
+  double* R = sm;          // [4][NA]: u (TMA)
   double* F = sm + kAdvF;  // [8][NA]: inv2a f, inv2a g
   const int x0 = (blockIdx.x % tiles_x) * TX, y0 = (blockIdx.x / tiles_x) * TY;
   const int parity = c->parity;
@@ -508,7 +509,7 @@ __global__ void __launch_bounds__(tiled::NT, 2)
   }
   mbar_wait(&bar, 0);
   if (!(x0 >= 2 && x0 + TX + 2 <= P.nx && y0 >= 1 && y0 + TY + 1 <= P.ny)) {
-    patch_box(P, src, rows, R, AX, AY, x0 - 2, y0 - 1, 0, 20, inv2a);
+    patch_box(P, src, rows, R, AX, AY, x0 - 2, y0 - 1, 0, 4, inv2a);
     __syncthreads();
   }
   for (int q = threadIdx.x; q < NA; q += NT) flux_cell(R, NA, F, NA, q, inv2a, gm1, false);
@@ -521,24 +522,32 @@ __global__ void __launch_bounds__(tiled::NT, 2)
   if (i < P.nx && j < P.ny) {
     auto rq = [](int x, int y) { return (y + 1) * AX + (x + 2); };
     auto M = [&](int q, int k) { return staged_m(R, NA, F, NA, q, k, w); };
-    auto pop = [&](int k, int q) { return plane4(R + (4 + 4 * k) * NA, NA, q); };
+    auto gpop = [&](int k, int ii, int jj) {  // interior: direct; ring: fill_ghosts values
+      if (ii >= 0 && ii < P.nx && jj >= 0 && jj < P.ny)
+        return load_plane4(src + (4 + 4 * k) * P.plane, P.plane, (long long)jj * P.pitch + ii);
+      return load_pop(P, src, rows, k, ii, jj, inv2a);
+    };
     double tw, te, ts, tn;
     face_thetas<kMode>(P, s, i, j, const_theta, tw, te, ts, tn);
     const long long off = (long long)j * P.pitch + i;
     const int qc = rq(tx, ty), qw = rq(tx - 1, ty), qe = rq(tx + 1, ty), qs = rq(tx, ty - 1),
               qn = rq(tx, ty + 1);
     const cs M0W = M(qw, 0), M1E = M(qe, 1), M2S = M(qs, 2), M3N = M(qn, 3);
-    const cs n1 = add(M0W, scale(tw, sub(M0W, pop(0, qw))));
-    const cs n2 = add(M1E, scale(te, sub(M1E, pop(1, qe))));
-    const cs n3 = add(M2S, scale(ts, sub(M2S, pop(2, qs))));
-    const cs n4 = add(M3N, scale(tn, sub(M3N, pop(3, qn))));
+    const cs n1 = add(M0W, scale(tw, sub(M0W, gpop(0, i - 1, j))));
+    const cs n2 = add(M1E, scale(te, sub(M1E, gpop(1, i + 1, j))));
+    const cs n3 = add(M2S, scale(ts, sub(M2S, gpop(2, i, j - 1))));
+    const cs n4 = add(M3N, scale(tn, sub(M3N, gpop(3, i, j + 1))));
     store_plane4(dst + 4 * P.plane, P.plane, off, n1);
     store_plane4(dst + 8 * P.plane, P.plane, off, n2);
     store_plane4(dst + 12 * P.plane, P.plane, off, n3);
     store_plane4(dst + 16 * P.plane, P.plane, off, n4);
     cs un = add(add(add(n1, n2), add(n3, n4)), scale(P.alpha, plane4(R, NA, qc)));
-    const cs out = add(add(scale(tw, sub(M(qc, 1), pop(1, qc))), scale(te, sub(M(qc, 0), pop(0, qc)))),
-                       add(scale(ts, sub(M(qc, 3), pop(3, qc))), scale(tn, sub(M(qc, 2), pop(2, qc)))));
+    const cs P0C = load_plane4(src + 4 * P.plane, P.plane, off);
+    const cs P1C = load_plane4(src + 8 * P.plane, P.plane, off);
+    const cs P2C = load_plane4(src + 12 * P.plane, P.plane, off);
+    const cs P3C = load_plane4(src + 16 * P.plane, P.plane, off);
+    const cs out = add(add(scale(tw, sub(M(qc, 1), P1C)), scale(te, sub(M(qc, 0), P0C))),
+                       add(scale(ts, sub(M(qc, 3), P3C)), scale(tn, sub(M(qc, 2), P2C))));
     un = sub(un, out);
     store_plane4(dst, P.plane, off, un);
     const double sp = signal_speed(un, P.gamma, gm1, P.conservative);
@@ -602,7 +611,7 @@ int encode_tensor_maps(MarchParams& P) {
   const cuuint64_t strides[3] = {(cuuint64_t)P.pitch * 8, (cuuint64_t)P.plane * 8,
                                  (cuuint64_t)P.sample_stride * 8};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
-  const cuuint32_t box_adv[4] = {tiled::AX, tiled::AY, 20, 1};
+  const cuuint32_t box_adv[4] = {tiled::AX, tiled::AY, 4, 1};
   const cuuint32_t box_thu[4] = {tiled::RX2, tiled::RY2, 4, 1};
   const cuuint32_t box_thp[4] = {tiled::AX, tiled::AY, 16, 1};
   for (int b = 0; b < 2; ++b) {
