@@ -276,7 +276,9 @@ def main():
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         ev0.record(stream)
+        torch.cuda.nvtx.range_push("timed")  # ncu --nvtx-include timed/ (tools/kprof.sh)
         sim.step(args.steps)
+        torch.cuda.nvtx.range_pop()
         ev1.record(stream)
         torch.cuda.synchronize()
     barrier()

@@ -194,12 +194,19 @@ void* vlbm_batch_stream(vlbm_batch* b);
 int vlbm_batch_set_timing(vlbm_batch* b, int enable);
 int vlbm_batch_stats(vlbm_batch* b, int64_t* launches, double* ms_theta, double* ms_advance,
                      double* ms_sched, int64_t* cell_updates);
-/* Audit of the limiter's certified bisection (test hook): when enabled, every
- * certified bisection step also runs the full 16-check feasible() and counts
- * disagreements.  vlbm_batch_audit fills counters[8]: disagreements (must be
- * 0), bisections entered, fully certified at the closed-form theta,
- * uncertified, not certifiable, no margin at theta = 0, uncertified vertices
- * at the start (sum), vertex evaluations in the bisections (sum). */
+/* Audit of the limiter's certificates (test hook): when enabled, every
+ * certified decision (the theta = 1 vertex certificate and each certified
+ * bisection step) is re-checked with the full 16-check feasible() and
+ * disagreements are counted.  vlbm_batch_audit fills
+ * counters[VLBM_AUDIT_COUNTERS]: disagreements (must be 0), bisections
+ * entered, fully certified at the closed-form theta, uncertified, not
+ * certifiable, no margin at theta = 0, uncertified vertices at the start
+ * (sum), vertex evaluations in the bisections (sum), cells whose diagonal
+ * passes at theta = 1, of those vertex-certified, of those feasible(1),
+ * warps with vertex checks left, and three certificate statistics
+ * (uncertified-but-feasible; of those with the true vertex minimum above
+ * p_FO / 2; of those with the quadratic part dominant). */
+#define VLBM_AUDIT_COUNTERS 16
 int vlbm_batch_set_audit(vlbm_batch* b, int enable);
 int vlbm_batch_audit(vlbm_batch* b, int64_t* counters);
 

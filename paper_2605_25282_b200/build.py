@@ -8,6 +8,7 @@ build), IEEE div/sqrt (nvcc defaults; never --use_fast_math).
 from __future__ import annotations
 
 import os
+import shlex
 import shutil
 import subprocess
 import sys
@@ -25,7 +26,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + [
     "-O3", "--fmad=false", "-prec-div=true", "-prec-sqrt=true", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC,-ffp-contract=off", "--expt-relaxed-constexpr", "-I", INCLUDE,
-]
+] + shlex.split(os.environ.get("VLBM_NVCC_EXTRA", ""))  # experiment hook (tools/ab variants)
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math", "-I", INCLUDE,
              "-I", "/usr/local/cuda/include"]
 

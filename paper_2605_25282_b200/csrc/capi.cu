@@ -112,6 +112,7 @@ void free_batch(vlbm_batch* b) {
   cudaFree(b->d_face_tx);
   cudaFree(b->d_face_ty);
   cudaFree(b->P.audit);
+  cudaFree(b->P.cert_hint);
   if (b->h_active) cudaFreeHost(b->h_active);
   for (cudaEvent_t e : b->ev) cudaEventDestroy(e);
   if (b->stream) cudaStreamDestroy(b->stream);
@@ -181,6 +182,13 @@ int alloc_batch(const vlbm_grid* g, const vlbm_params* p, int S, int device, vlb
   // ranges: offset pointers, own control slice, limiter queues, tensor maps,
   // counter and stream), so one group's HBM-bound advance overlaps another
   // group's FP64-bound limiter.  VLBM_GROUPS overrides the default.
+  P.cert1 = 1;
+  if (const char* e = getenv("VLBM_CERT1")) P.cert1 = atoi(e) != 0;
+  {
+    const size_t n = (size_t)S * vlbm_impl::theta_tiles(P.nx, P.ny) * 8;
+    chk(cudaMalloc(&P.cert_hint, n), "malloc cert_hint");
+    if (rc == VLBM_OK) chk(cudaMemset(P.cert_hint, 3, n), "memset cert_hint");
+  }
   int G = S >= 8 ? 2 : 1;
   if (const char* e = getenv("VLBM_GROUPS")) G = std::max(1, std::min(S, atoi(e)));
   b->G = G;
@@ -204,6 +212,7 @@ int alloc_batch(const vlbm_grid* g, const vlbm_params* p, int S, int device, vlb
     Q.theta = P.theta + (size_t)s0 * P.plane;
     Q.inlet = P.inlet + (size_t)s0 * P.ny * 4;
     Q.n_active = b->d_active_g + g;
+    Q.cert_hint = P.cert_hint + (size_t)s0 * vlbm_impl::theta_tiles(P.nx, P.ny) * 8;
     cudaStream_t sg = b->stream;
     if (g > 0) chk(cudaStreamCreateWithFlags(&sg, cudaStreamNonBlocking), "stream g");
     if (p->limiter == VLBM_LIMITER_RLMP) {
@@ -595,8 +604,8 @@ int vlbm_batch_set_audit(vlbm_batch* b, int enable) {
   if (!b) return set_error(VLBM_E_INVALID, "null batch");
   CU(cudaSetDevice(b->device));
   if (enable && !b->P.audit) {
-    CU(cudaMalloc(&b->P.audit, 8 * sizeof(int)));
-    CU(cudaMemset(b->P.audit, 0, 8 * sizeof(int)));
+    CU(cudaMalloc(&b->P.audit, VLBM_AUDIT_COUNTERS * sizeof(int)));
+    CU(cudaMemset(b->P.audit, 0, VLBM_AUDIT_COUNTERS * sizeof(int)));
   } else if (!enable && b->P.audit) {
     CU(cudaFree(b->P.audit));
     b->P.audit = nullptr;
@@ -607,12 +616,12 @@ int vlbm_batch_set_audit(vlbm_batch* b, int enable) {
 
 int vlbm_batch_audit(vlbm_batch* b, int64_t* counters) {
   if (!b || !counters) return set_error(VLBM_E_INVALID, "null argument");
-  int h[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int h[VLBM_AUDIT_COUNTERS] = {};
   if (b->P.audit) {
     CU(cudaMemcpyAsync(h, b->P.audit, sizeof(h), cudaMemcpyDeviceToHost, b->stream));
     CU(cudaStreamSynchronize(b->stream));
   }
-  for (int k = 0; k < 8; ++k) counters[k] = h[k];
+  for (int k = 0; k < VLBM_AUDIT_COUNTERS; ++k) counters[k] = h[k];
   return VLBM_OK;
 }
 

@@ -40,6 +40,8 @@ cudaError_t launch_advance(const vlbm_dev::MarchParams& P, int mode, double cons
 // tiled production kernels (march_tiled.cu)
 int encode_tensor_maps(vlbm_dev::MarchParams& P);
 cudaError_t launch_theta_tiled(const vlbm_dev::MarchParams& P, cudaStream_t st);
+// Tiles of k_theta_tiled's grid (32 x 8 cells each) per sample.
+inline int theta_tiles(int nx, int ny) { return ((nx + 31) / 32) * ((ny + 7) / 8); }
 cudaError_t launch_advance_tiled(const vlbm_dev::MarchParams& P, int mode, double const_theta,
                                  cudaStream_t st);
 cudaError_t launch_set_budget(const vlbm_dev::MarchParams& P, long long budget,

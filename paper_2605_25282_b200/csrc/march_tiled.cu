@@ -29,6 +29,7 @@
 #include "rlmp.cuh"
 
 namespace vlbm_dev {
+constexpr int kCertProbe = 8;  // steps between re-probes of a warp's certificate
 namespace tiled {
 constexpr int TX = 32, TY = 8, NT = TX * TY;
 constexpr int RX2 = TX + 4, RY2 = TY + 4, NR2 = RX2 * RY2;  // limiter u box (halo 2): 36 x 12
@@ -156,6 +157,61 @@ __device__ __forceinline__ cs staged_m(const double* U, int NU, const double* F,
   return (k & 1) ? sub(wu, a) : add(wu, a);
 }
 
+// Slot of this thread among the flagged threads of the CTA: warp ballot, one
+// shared atomic per warp.  All threads call it.
+__device__ __forceinline__ int block_slot(bool flag, int* counter) {
+  const unsigned lane = threadIdx.x & 31;
+  const unsigned m = __ballot_sync(0xffffffffu, flag);
+  int slot = 0;
+  if (m) {
+    const int leader = __ffs(m) - 1;
+    int wb = 0;
+    if ((int)lane == leader) wb = atomicAdd(counter, __popc(m));
+    wb = __shfl_sync(0xffffffffu, wb, leader);
+    slot = wb + __popc(m & ((1u << lane) - 1u));
+  }
+  return slot;
+}
+
+// Append the CTA's hard cells (flag) to the global limiter queue: block-
+// aggregated slots, one global atomic per CTA.  When the queue is full (or
+// absent) the cell finishes in place.  All threads call it.
+__device__ __forceinline__ void enqueue_hard(const MarchParams& P, bool hard, long long cell,
+                                             const cs& fo, const cs* cf, const RlmpBounds& b,
+                                             double gm1, int& qn, int& qbase) {
+  __syncthreads();
+  if (threadIdx.x == 0) qn = 0;
+  __syncthreads();
+  const int slot = block_slot(hard, &qn);
+  __syncthreads();
+  if (threadIdx.x == 0) qbase = (qn && P.hq) ? atomicAdd(P.hq_n, qn) : 0;
+  __syncthreads();
+  if (!hard) return;
+  if (P.hq && qbase + qn <= P.hq_cap) {
+    const long long cap = P.hq_cap;
+    double* q = P.hq + qbase + slot;
+    q[0] = fo.r;
+    q[cap] = fo.mx;
+    q[2 * cap] = fo.my;
+    q[3 * cap] = fo.e;
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+      q[(4 + 4 * f) * cap] = cf[f].r;
+      q[(5 + 4 * f) * cap] = cf[f].mx;
+      q[(6 + 4 * f) * cap] = cf[f].my;
+      q[(7 + 4 * f) * cap] = cf[f].e;
+    }
+    q[20 * cap] = b.rho_lo;
+    q[21 * cap] = b.rho_hi;
+    q[22 * cap] = b.p_lo;
+    q[23 * cap] = b.p_hi;
+    P.hq_idx[qbase + slot] = cell;
+  } else {  // queue full (or absent): finish in place
+    if (P.hq && qbase + slot < P.hq_cap) P.hq_idx[qbase + slot] = -1;
+    P.theta[cell] = rlmp_theta_hard(fo, cf, b, gm1, P.audit);
+  }
+}
+
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(tiled::NT, 2)
     k_theta_tiled(MarchParams P, int tiles_x, const __grid_constant__ CUtensorMap tmu0,
@@ -208,7 +264,7 @@ __global__ void __launch_bounds__(tiled::NT, 2)
     return add(add(a, b), scale(al, plane4(R, NR2, rq(x, y))));
   };
   const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
-  const cs foC = ufo_at(tx, ty);
+  cs foC = ufo_at(tx, ty);
   RF[fq(tx, ty)] = foC.r;
   RF[NF + fq(tx, ty)] = pressure(foC, gm1);
   if (threadIdx.x < 2 * TX + 2 * TY) {
@@ -235,7 +291,13 @@ __global__ void __launch_bounds__(tiled::NT, 2)
   const bool valid = i < P.nx && j < P.ny;
   cs cf[4];
   RlmpBounds b;
-  bool hard = false;
+  bool hard = false, need = false;
+  // Certificate hint of this warp (warp-uniform), see MarchParams::cert_hint.
+  unsigned char* hint =
+      P.cert_hint ? P.cert_hint + ((long long)s * gridDim.x + blockIdx.x) * 8 + (threadIdx.x >> 5)
+                  : nullptr;
+  const int h0 = hint ? *hint : 3;
+  const bool try_cert = P.cert1 && (h0 >= 2 || (c->steps % kCertProbe) == 0);
   if (valid) {
     auto pop = [&](int k, int x, int y) {
       return plane4(SP + 4 * k * NA, NA, (y + 1) * AX + (x + 2));
@@ -262,50 +324,49 @@ __global__ void __launch_bounds__(tiled::NT, 2)
     }
     b = rlmp_bounds(st, P.kappa, P.rho_floor_coef, P.p_floor_coef);
     const cs delta = add(add(cf[0], cf[1]), add(cf[2], cf[3]));
-    if (feasible(1.0, foC, delta, cf, b, gm1))
-      P.theta[(long long)s * P.plane + (long long)j * P.pitch + i] = 1.0;
-    else
+    // feasible(1): the diagonal first; the 15 vertex floors only when the
+    // certificate cannot prove them.
+    if (diag_ok(1.0, foC, delta, b, gm1)) {
+      double parts[2] = {0.0, 0.0};
+      const bool cert = try_cert && vertices_certified_at_one(foC, st.pfo[0], cf, b.rho_floor,
+                                                             b.p_floor, gm1,
+                                                             P.audit ? parts : nullptr);
+      need = !cert;
+      const bool ok = cert || vertex_floors_ok(1.0, foC, cf, b, gm1);
+      if (P.audit) {  // [8] diagonal passed, [9] certified, [10] feasible; [0] certificate errors
+        atomicAdd(P.audit + 8, 1);
+        if (cert) atomicAdd(P.audit + 9, 1);
+        if (ok) atomicAdd(P.audit + 10, 1);
+        if (cert && !vertex_floors_ok(1.0, foC, cf, b, gm1)) atomicAdd(P.audit, 1);
+        if (!cert && ok) {
+          // [12] uncertified but feasible; [13] of those the true vertex
+          // minimum is above p_FO / 2 (bound loose); [14] quadratic part
+          // dominates the bound
+          double pmin = st.pfo[0];
+          for (int mask = 1; mask < 16; ++mask)
+            pmin = smin(pmin, pressure(vertex_at(foC, cf, mask), gm1));
+          atomicAdd(P.audit + 12, 1);
+          if (pmin > 0.5 * st.pfo[0]) atomicAdd(P.audit + 13, 1);
+          if (parts[1] > parts[0]) atomicAdd(P.audit + 14, 1);
+        }
+      }
+      if (ok)
+        P.theta[(long long)s * P.plane + (long long)j * P.pitch + i] = 1.0;
+      else
+        hard = true;
+    } else {
       hard = true;
-  }
-  // Hard cells: warp-aggregated slots in this CTA, one global atomic per CTA.
-  const unsigned lane = threadIdx.x & 31;
-  const unsigned m = __ballot_sync(0xffffffffu, hard);
-  int slot = 0;
-  if (m) {
-    const int leader = __ffs(m) - 1;
-    int wb = 0;
-    if ((int)lane == leader) wb = atomicAdd(&qn, __popc(m));
-    wb = __shfl_sync(0xffffffffu, wb, leader);
-    slot = wb + __popc(m & ((1u << lane) - 1u));
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) qbase = (qn && P.hq) ? atomicAdd(P.hq_n, qn) : 0;
-  __syncthreads();
-  if (!hard) return;
-  const long long cell = (long long)s * P.plane + (long long)j * P.pitch + i;
-  if (P.hq && qbase + qn <= P.hq_cap) {
-    const long long cap = P.hq_cap;
-    double* q = P.hq + qbase + slot;
-    q[0] = foC.r;
-    q[cap] = foC.mx;
-    q[2 * cap] = foC.my;
-    q[3 * cap] = foC.e;
-#pragma unroll
-    for (int f = 0; f < 4; ++f) {
-      q[(4 + 4 * f) * cap] = cf[f].r;
-      q[(5 + 4 * f) * cap] = cf[f].mx;
-      q[(6 + 4 * f) * cap] = cf[f].my;
-      q[(7 + 4 * f) * cap] = cf[f].e;
     }
-    q[20 * cap] = b.rho_lo;
-    q[21 * cap] = b.rho_hi;
-    q[22 * cap] = b.p_lo;
-    q[23 * cap] = b.p_hi;
-    P.hq_idx[qbase + slot] = cell;
-  } else {  // queue full (or absent): finish in place
-    if (P.hq && qbase + slot < P.hq_cap) P.hq_idx[qbase + slot] = -1;
-    P.theta[cell] = rlmp_theta_hard(foC, cf, b, gm1, P.audit);
   }
+  {
+    const unsigned m = __ballot_sync(0xffffffffu, need);
+    if ((threadIdx.x & 31) == 0) {
+      if (hint && try_cert) *hint = (unsigned char)(m == 0 ? min(h0 + 1, 3) : max(h0 - 1, 0));
+      if (P.audit && m) atomicAdd(P.audit + 11, 1);  // [11] warps with vertex checks left
+    }
+  }
+  const long long cell = (long long)s * P.plane + (long long)j * P.pitch + i;
+  enqueue_hard(P, hard, cell, foC, cf, b, gm1, qn, qbase);
 }
 
 // The limiter's hard cells, in three convergent passes (the rest of
@@ -583,6 +644,7 @@ static cudaError_t smem_attrs() {
   return done;
 }
 
+static_assert(tiled::TX == 32 && tiled::TY == 8 && tiled::NT == 256, "theta_tiles() layout");
 static dim3 tiled_grid(const MarchParams& P, int& tiles_x) {
   tiles_x = (P.nx + tiled::TX - 1) / tiled::TX;
   const int ty = (P.ny + tiled::TY - 1) / tiled::TY;

@@ -31,7 +31,7 @@ from typing import Sequence
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libvlbm_b200.so")
+LIB_PATH = os.environ.get("VLBM_LIB") or os.path.join(_PKG, "lib", "libvlbm_b200.so")
 
 D, I, U64, I64 = C.c_double, C.c_int, C.c_uint64, C.c_int64
 DP = C.POINTER(C.c_double)
@@ -381,11 +381,13 @@ class BatchSimulation:
         _check(lib().vlbm_batch_set_audit(self._h, int(on)))
 
     def audit_counters(self) -> dict:
-        n = (I64 * 8)()
+        n = (I64 * 16)()
         _check(lib().vlbm_batch_audit(self._h, n))
         return dict(mismatches=n[0], bisections=n[1], certified_at_thc=n[2], uncertified=n[3],
                     not_certifiable=n[4], no_margin_at_0=n[5], unc_vertices_start=n[6],
-                    vertex_evals=n[7])
+                    vertex_evals=n[7], diag_ok_at_1=n[8], vertex_certified_at_1=n[9],
+                    feasible_at_1=n[10], warps_with_vertex_checks=n[11],
+                    unc_feasible=n[12], unc_feasible_loose=n[13], unc_feasible_quad=n[14])
 
     def audit_mismatches(self) -> int:
         return self.audit_counters()["mismatches"]
