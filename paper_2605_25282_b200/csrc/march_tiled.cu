@@ -28,6 +28,15 @@
 #include "march_common.cuh"
 #include "rlmp.cuh"
 
+#ifndef VLBM_THETA_GPOP
+#define VLBM_THETA_GPOP 0  // 1: limiter reads populations from global (no SP stage)
+#endif
+#ifndef VLBM_THETA_MINB
+#define VLBM_THETA_MINB 2
+#endif
+#ifndef VLBM_ADV_MINB
+#define VLBM_ADV_MINB 4  // resident advance CTAs per SM (register budget)
+#endif
 namespace vlbm_dev {
 constexpr int kCertProbe = 8;  // steps between re-probes of a warp's certificate
 namespace tiled {
@@ -41,8 +50,9 @@ constexpr int AX = TX + 4, AY = TY + 2, NA = AX * AY;        // 36 x 10
 constexpr int kStagedTheta = 13;  // u(4) [TMA], inv2a*f(4), inv2a*g(4), p
 // limiter smem: R [13][NR2] | RF [2][NF] | pad | SP [16][NA] (TMA, 128-B aligned)
 constexpr int kThetaSP = ((kStagedTheta * NR2 + 2 * NF) + 15) / 16 * 16;
-constexpr size_t kThetaSmem = sizeof(double) * (kThetaSP + 16 * NA);
-constexpr unsigned kThetaTx = sizeof(double) * (4 * NR2 + 16 * NA);
+constexpr int kThetaSPn = VLBM_THETA_GPOP ? 0 : 16 * NA;
+constexpr size_t kThetaSmem = sizeof(double) * (kThetaSP + kThetaSPn);
+constexpr unsigned kThetaTx = sizeof(double) * (4 * NR2 + kThetaSPn);
 // advance smem: R [4][NA] (TMA: u) | F [8][NA] (inv2a f, inv2a g); the
 // populations are read from global memory by their pulling thread.
 constexpr int kAdvF = 4 * NA;
@@ -213,7 +223,7 @@ __device__ __forceinline__ void enqueue_hard(const MarchParams& P, bool hard, lo
 }
 
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(tiled::NT, 2)
+__global__ void __launch_bounds__(tiled::NT, VLBM_THETA_MINB)
     k_theta_tiled(MarchParams P, int tiles_x, const __grid_constant__ CUtensorMap tmu0,
                   const __grid_constant__ CUtensorMap tmu1, const __grid_constant__ CUtensorMap tmp0,
                   const __grid_constant__ CUtensorMap tmp1) {
@@ -241,12 +251,12 @@ __global__ void __launch_bounds__(tiled::NT, 2)
   if (threadIdx.x == 0) {
     mbar_expect_tx(&bar, kThetaTx);
     tma_load_4d(R, parity ? &tmu1 : &tmu0, &bar, x0 - 2, y0 - 2, 0, s);
-    tma_load_4d(SP, parity ? &tmp1 : &tmp0, &bar, x0 - 2, y0 - 1, 4, s);
+    if (!VLBM_THETA_GPOP) tma_load_4d(SP, parity ? &tmp1 : &tmp0, &bar, x0 - 2, y0 - 1, 4, s);
   }
   mbar_wait(&bar, 0);
   if (!(x0 >= 2 && x0 + TX + 2 <= P.nx && y0 >= 2 && y0 + TY + 2 <= P.ny)) {
     patch_box(P, src, rows, R, RX2, RY2, x0 - 2, y0 - 2, 0, 4, inv2a);
-    patch_box(P, src, rows, SP, AX, AY, x0 - 2, y0 - 1, 4, 16, inv2a);
+    if (!VLBM_THETA_GPOP) patch_box(P, src, rows, SP, AX, AY, x0 - 2, y0 - 1, 4, 16, inv2a);
     __syncthreads();
   }
   double* F = R + 4 * NR2;
@@ -300,6 +310,12 @@ __global__ void __launch_bounds__(tiled::NT, 2)
   const bool try_cert = P.cert1 && (h0 >= 2 || (c->steps % kCertProbe) == 0);
   if (valid) {
     auto pop = [&](int k, int x, int y) {
+      if (VLBM_THETA_GPOP) {
+        const int ii = x0 + x, jj = y0 + y;
+        if (ii >= 0 && ii < P.nx && jj >= 0 && jj < P.ny)
+          return load_plane4(src + (4 + 4 * k) * P.plane, P.plane, (long long)jj * P.pitch + ii);
+        return load_pop(P, src, rows, k, ii, jj, inv2a);
+      }
       return plane4(SP + 4 * k * NA, NA, (y + 1) * AX + (x + 2));
     };
     const int qc = rq(tx, ty);
@@ -543,7 +559,7 @@ __global__ void __launch_bounds__(256, 2) k_bisect_unc(MarchParams P) {
 
 // ---------------------------------------------------------------------------
 template <int kMode>
-__global__ void __launch_bounds__(tiled::NT, 3)
+__global__ void __launch_bounds__(tiled::NT, VLBM_ADV_MINB)
     k_advance_tiled(MarchParams P, double const_theta, int tiles_x,
                     const __grid_constant__ CUtensorMap tma0,
                     const __grid_constant__ CUtensorMap tma1) {
