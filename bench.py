@@ -36,7 +36,10 @@ sys.path.insert(0, ROOT)
 
 NX, NY, M_PER_GPU = 1000, 200, 64
 BYTES_PER_UPDATE = 320      # read u(4)+pops(16) f64, write the same
-THETA_BYTES_PER_CELL = 168  # k_theta: read u + pops (160 B), write theta (8 B)
+THETA_BYTES_PER_CELL = 168  # k_theta_tiled: read u + pops (160 B), write theta (8 B)
+# FP64 peak of the non-tensor pipe, counting DADD/DMUL/DFMA as one instruction
+# (the march is built with --fmad=false): 148 SMs x 64 FP64 lanes x 1.965 GHz.
+FP64_PEAK_TINST = 148 * 64 * 1.965e9 / 1e12
 
 
 def peaks():
@@ -96,6 +99,16 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
                 "samples": len(self.rows)}
+
+
+def fp64_profile():
+    """FP64 thread instructions per cell of the limiter kernels, from the
+    committed ncu capture (profiles/r1_fp64.json, made by tools/profile_r1.sh)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_fp64.json")) as f:
+            return json.load(f)
+    except Exception:
+        return None
 
 
 def dist_env():
@@ -238,6 +251,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-postproc", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-roofline", action="store_true",
+                    help="skip the one-group per-kernel timing pass")
     ap.add_argument("--ref-seconds", type=float, default=15.0,
                     help="target CPU seconds of the reference-CPU sample")
     args = ap.parse_args()
@@ -302,6 +317,26 @@ def main():
     value = upd_total / (t_max * 1e-3)
     sim.close()
 
+    # ---- per-kernel device times for the roofline: the same step window
+    # marched again with one sample group, so no two march kernels overlap
+    # and each launch's CUDA-event time is its own duration.
+    kern = None
+    if not args.no_roofline:
+        os.environ["VLBM_GROUPS"] = "1"
+        r = v.BatchSimulation.jet(g, lat, gas, pp, base_seed=42, m0=rank * M, n_samples=M,
+                                  device=local)
+        del os.environ["VLBM_GROUPS"]
+        if args.t_start > 0:
+            r.run_to(args.t_start)
+        r.step(args.warmup)
+        r.set_timing(True)
+        k0 = r.stats()
+        r.step(args.steps)
+        k1 = r.stats()
+        r.close()
+        kern = {k: (k1[k] - k0[k]) / args.steps for k in
+                ("ms_theta_tiles", "ms_theta_hard", "ms_advance", "ms_sched")}
+
     # ---- e2e through the public API from host buffers ----
     e2e = None
     if not args.no_e2e:
@@ -338,8 +373,28 @@ def main():
     if rank == 0:
         hbm, src = peaks()
         cells_per_launch = M * NX * NY
-        achieved = THETA_BYTES_PER_CELL * cells_per_launch / (theta_ms * 1e-3) / 1e9
         step_gbs = BYTES_PER_UPDATE * (updates / (ms * 1e-3)) / 1e9
+        roof, fp64 = None, None
+        if kern:
+            t_tiles = kern["ms_theta_tiles"] * 1e-3
+            achieved = THETA_BYTES_PER_CELL * cells_per_launch / t_tiles / 1e9
+            roof = {"bound": "hbm", "kernel": "k_theta_tiled", "achieved": achieved, "peak": hbm,
+                    "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                    "peak_source": src, "bytes_per_cell": THETA_BYTES_PER_CELL,
+                    "launch_ms": kern["ms_theta_tiles"],
+                    "note": "dominant kernel is FP64-bound, see fp64_roofline; per-launch "
+                            "times from a one-group pass over the same step window"}
+            prof = fp64_profile()
+            if prof:
+                roof["traffic"] = prof.get("k_theta_tiled_dram_bytes_per_launch")
+                ops = prof["k_theta_tiled_fp64_inst_per_cell"]
+                fp64 = {"kernel": "k_theta_tiled", "achieved": ops * cells_per_launch / t_tiles
+                        / 1e12, "peak": FP64_PEAK_TINST, "unit": "Tinst/s",
+                        "frac": ops * cells_per_launch / t_tiles / 1e12 / FP64_PEAK_TINST,
+                        "fp64_inst_per_cell": ops, "source": prof.get("source")}
+            adv_gbs = BYTES_PER_UPDATE * cells_per_launch / (kern["ms_advance"] * 1e-3) / 1e9
+            kern["advance_hbm"] = {"achieved": adv_gbs, "peak": hbm, "unit": "GB/s",
+                                   "frac": adv_gbs / hbm, "bytes_per_cell": BYTES_PER_UPDATE}
         line = {
             "metric": "VLBM sample-cell updates/s (GLUPS) & % HBM roofline; W1 post-proc cells/s",
             "value": value, "unit": "sample-cell-updates/s", "n_gpus": ws,
@@ -352,14 +407,13 @@ def main():
                        "l2": "inputs larger than L2 (4.1 GB state per GPU)"},
             "glups": value / 1e9,
             "gpu_launches": launches,
-            "roofline": {"bound": "hbm", "kernel": "k_theta", "achieved": achieved, "peak": hbm,
-                         "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
-                         "peak_source": src,
-                         "bytes_per_cell": THETA_BYTES_PER_CELL,
-                         "note": "RLMP limiter is FP64-bound; see fp64 + step keys"},
+            "roofline": roof,
+            "fp64_roofline": fp64,
             "step_roofline": {"achieved": step_gbs, "peak": hbm, "unit": "GB/s",
                               "frac": step_gbs / hbm, "bytes_per_update": BYTES_PER_UPDATE},
-            "kernel_ms_per_step": {"k_theta": theta_ms, "k_advance": adv_ms, "k_sched": sched_ms},
+            "kernel_ms_per_step": {"k_theta": theta_ms, "k_advance": adv_ms, "k_sched": sched_ms,
+                                   "note": "timed region (2 sample groups overlap)"},
+            "kernel_ms_per_step_1group": kern,
             "clocks": clk.summary(),
         }
         if e2e:

@@ -194,6 +194,11 @@ void* vlbm_batch_stream(vlbm_batch* b);
 int vlbm_batch_set_timing(vlbm_batch* b, int enable);
 int vlbm_batch_stats(vlbm_batch* b, int64_t* launches, double* ms_theta, double* ms_advance,
                      double* ms_sched, int64_t* cell_updates);
+/* The timed device ms by kernel group: ms[0] limiter tile pass (u_FO, bounds,
+ * feasible(1)), ms[1] limiter hard cells (cap + bisections), ms[2] advance,
+ * ms[3] scheduler.  With several sample groups the groups' overlapping
+ * launches are each timed on their own stream. */
+int vlbm_batch_kernel_ms(vlbm_batch* b, double* ms);
 /* Audit of the limiter's certificates (test hook): when enabled, every
  * certified decision (the theta = 1 vertex certificate and each certified
  * bisection step) is re-checked with the full 16-check feasible() and

@@ -56,9 +56,9 @@ struct vlbm_batch {
   // stats
   bool timing = false;
   long long launches = 0;
-  double ms_theta = 0, ms_advance = 0, ms_sched = 0;
+  double ms_kind[4] = {0, 0, 0, 0};  // sched, limiter tile pass, advance, limiter hard path
   std::vector<cudaEvent_t> ev;  // pool of events, pairs per timed launch
-  std::vector<int> ev_kind;     // 0 sched, 1 theta, 2 advance
+  std::vector<int> ev_kind;     // index into ms_kind
   std::vector<cudaStream_t> ev_stream;
   int ev_used = 0;
   // sample groups (march views), see alloc_batch
@@ -310,12 +310,7 @@ void harvest(vlbm_batch* b) {
   for (int q = 0; q < b->ev_used; ++q) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, b->ev[2 * q], b->ev[2 * q + 1]);
-    if (b->ev_kind[q] == 0)
-      b->ms_sched += ms;
-    else if (b->ev_kind[q] == 1)
-      b->ms_theta += ms;
-    else
-      b->ms_advance += ms;
+    b->ms_kind[b->ev_kind[q]] += ms;
   }
   b->ev_used = 0;
 }
@@ -343,7 +338,10 @@ int march_loop(vlbm_batch* b, double target, double fixed_dt, int mode, int chun
         record_end(b);
         if (rlmp) {
           record(b, 1, st);
-          CU(vlbm_impl::launch_theta(Q, st));
+          CU(vlbm_impl::launch_theta(Q, st, 0));
+          record_end(b);
+          record(b, 3, st);
+          CU(vlbm_impl::launch_theta(Q, st, 1));
           record_end(b);
         }
         record(b, 2, st);
@@ -596,7 +594,7 @@ void* vlbm_batch_stream(vlbm_batch* b) { return b ? (void*)b->stream : nullptr; 
 int vlbm_batch_set_timing(vlbm_batch* b, int enable) {
   if (!b) return set_error(VLBM_E_INVALID, "null batch");
   b->timing = enable != 0;
-  b->ms_theta = b->ms_advance = b->ms_sched = 0;
+  for (double& m : b->ms_kind) m = 0;
   return VLBM_OK;
 }
 
@@ -625,13 +623,22 @@ int vlbm_batch_audit(vlbm_batch* b, int64_t* counters) {
   return VLBM_OK;
 }
 
+int vlbm_batch_kernel_ms(vlbm_batch* b, double* ms) {
+  if (!b || !ms) return set_error(VLBM_E_INVALID, "null argument");
+  ms[0] = b->ms_kind[1];
+  ms[1] = b->ms_kind[3];
+  ms[2] = b->ms_kind[2];
+  ms[3] = b->ms_kind[0];
+  return VLBM_OK;
+}
+
 int vlbm_batch_stats(vlbm_batch* b, int64_t* launches, double* ms_theta, double* ms_advance,
                      double* ms_sched, int64_t* cell_updates) {
   if (!b) return set_error(VLBM_E_INVALID, "null batch");
   if (launches) *launches = b->launches;
-  if (ms_theta) *ms_theta = b->ms_theta;
-  if (ms_advance) *ms_advance = b->ms_advance;
-  if (ms_sched) *ms_sched = b->ms_sched;
+  if (ms_theta) *ms_theta = b->ms_kind[1] + b->ms_kind[3];
+  if (ms_advance) *ms_advance = b->ms_kind[2];
+  if (ms_sched) *ms_sched = b->ms_kind[0];
   if (cell_updates) {
     std::vector<SampleCtl> ctl;
     if (int rc = read_ctl(b, ctl)) return rc;

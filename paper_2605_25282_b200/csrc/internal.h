@@ -33,13 +33,16 @@ cudaError_t launch_signal(const vlbm_dev::MarchParams& P, cudaStream_t st);
 cudaError_t launch_init(const vlbm_dev::MarchParams& P, double* d_a0, cudaStream_t st);
 cudaError_t launch_sched(const vlbm_dev::MarchParams& P, double target, double fixed_dt,
                          cudaStream_t st);
-cudaError_t launch_theta(const vlbm_dev::MarchParams& P, cudaStream_t st);
+// part 0: the tile pass (u_FO, bounds, feasible(1), hard-cell queue);
+// part 1: the hard cells (closed-form cap, certified bisections).
+cudaError_t launch_theta(const vlbm_dev::MarchParams& P, cudaStream_t st, int part);
 // mode 0: cell theta plane, 1: constant theta, 2: prescribed faces
 cudaError_t launch_advance(const vlbm_dev::MarchParams& P, int mode, double const_theta,
                            cudaStream_t st);
 // tiled production kernels (march_tiled.cu)
 int encode_tensor_maps(vlbm_dev::MarchParams& P);
 cudaError_t launch_theta_tiled(const vlbm_dev::MarchParams& P, cudaStream_t st);
+cudaError_t launch_theta_hard(const vlbm_dev::MarchParams& P, cudaStream_t st);
 // Tiles of k_theta_tiled's grid (32 x 8 cells each) per sample.
 inline int theta_tiles(int nx, int ny) { return ((nx + 31) / 32) * ((ny + 7) / 8); }
 cudaError_t launch_advance_tiled(const vlbm_dev::MarchParams& P, int mode, double const_theta,

@@ -381,12 +381,12 @@ static bool use_v0() {
   return v != 0;
 }
 
-cudaError_t launch_theta(const MarchParams& P, cudaStream_t st) {
+cudaError_t launch_theta(const MarchParams& P, cudaStream_t st, int part) {
   if (use_v0()) {
-    k_theta<<<tile_grid(P), 256, 0, st>>>(P);
+    if (part == 0) k_theta<<<tile_grid(P), 256, 0, st>>>(P);
     return cudaGetLastError();
   }
-  return launch_theta_tiled(P, st);
+  return part == 0 ? launch_theta_tiled(P, st) : launch_theta_hard(P, st);
 }
 
 cudaError_t launch_advance(const MarchParams& P, int mode, double const_theta, cudaStream_t st) {

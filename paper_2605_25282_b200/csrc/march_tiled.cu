@@ -585,6 +585,8 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_ADV_MINB)
     tma_load_4d(R, parity ? &tma1 : &tma0, &bar, x0 - 2, y0 - 1, 0, s);
   }
   mbar_wait(&bar, 0);
+  // every cell of the tile has its four neighbours inside the domain
+  const bool interior = x0 >= 1 && x0 + TX + 1 <= P.nx && y0 >= 1 && y0 + TY + 1 <= P.ny;
   if (!(x0 >= 2 && x0 + TX + 2 <= P.nx && y0 >= 1 && y0 + TY + 1 <= P.ny)) {
     patch_box(P, src, rows, R, AX, AY, x0 - 2, y0 - 1, 0, 4, inv2a);
     __syncthreads();
@@ -605,15 +607,38 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_ADV_MINB)
       return load_pop(P, src, rows, k, ii, jj, inv2a);
     };
     double tw, te, ts, tn;
-    face_thetas<kMode>(P, s, i, j, const_theta, tw, te, ts, tn);
+    if (kMode == 0 && interior) {  // face_thetas without the boundary branches
+      const double* th = P.theta + (long long)s * P.plane + (long long)j * P.pitch + i;
+      const double tc = th[0];
+      tw = smin(th[-1], tc);
+      te = smin(tc, th[1]);
+      ts = smin(th[-P.pitch], tc);
+      tn = smin(tc, th[P.pitch]);
+    } else {
+      face_thetas<kMode>(P, s, i, j, const_theta, tw, te, ts, tn);
+    }
     const long long off = (long long)j * P.pitch + i;
     const int qc = rq(tx, ty), qw = rq(tx - 1, ty), qe = rq(tx + 1, ty), qs = rq(tx, ty - 1),
               qn = rq(tx, ty + 1);
+    // Pulled populations: on interior tiles (CTA-uniform test) the 16 loads
+    // sit in one branch-free block so they issue back to back.
+    cs pw, pe, ps, pn;
+    if (interior) {
+      pw = load_plane4(src + 4 * P.plane, P.plane, off - 1);
+      pe = load_plane4(src + 8 * P.plane, P.plane, off + 1);
+      ps = load_plane4(src + 12 * P.plane, P.plane, off - P.pitch);
+      pn = load_plane4(src + 16 * P.plane, P.plane, off + P.pitch);
+    } else {
+      pw = gpop(0, i - 1, j);
+      pe = gpop(1, i + 1, j);
+      ps = gpop(2, i, j - 1);
+      pn = gpop(3, i, j + 1);
+    }
     const cs M0W = M(qw, 0), M1E = M(qe, 1), M2S = M(qs, 2), M3N = M(qn, 3);
-    const cs n1 = add(M0W, scale(tw, sub(M0W, gpop(0, i - 1, j))));
-    const cs n2 = add(M1E, scale(te, sub(M1E, gpop(1, i + 1, j))));
-    const cs n3 = add(M2S, scale(ts, sub(M2S, gpop(2, i, j - 1))));
-    const cs n4 = add(M3N, scale(tn, sub(M3N, gpop(3, i, j + 1))));
+    const cs n1 = add(M0W, scale(tw, sub(M0W, pw)));
+    const cs n2 = add(M1E, scale(te, sub(M1E, pe)));
+    const cs n3 = add(M2S, scale(ts, sub(M2S, ps)));
+    const cs n4 = add(M3N, scale(tn, sub(M3N, pn)));
     store_plane4(dst + 4 * P.plane, P.plane, off, n1);
     store_plane4(dst + 8 * P.plane, P.plane, off, n2);
     store_plane4(dst + 12 * P.plane, P.plane, off, n3);
@@ -717,6 +742,10 @@ cudaError_t launch_theta_tiled(const MarchParams& P, cudaStream_t st) {
   const dim3 g = tiled_grid(P, tx);
   k_theta_tiled<<<g, tiled::NT, tiled::kThetaSmem, st>>>(P, tx, P.tm_thu[0], P.tm_thu[1],
                                                           P.tm_thp[0], P.tm_thp[1]);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_theta_hard(const MarchParams& P, cudaStream_t st) {
   if (P.hq) {
     k_theta_hard<<<148 * 8, 256, 0, st>>>(P);
     k_bisect_cert<<<148 * 8, 256, 0, st>>>(P);

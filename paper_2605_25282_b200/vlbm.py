@@ -182,6 +182,7 @@ def lib() -> C.CDLL:
     sig("vlbm_batch_stream", V, [V])
     sig("vlbm_batch_set_timing", I, [V, I])
     sig("vlbm_batch_stats", I, [V, C.POINTER(I64), DP, DP, DP, C.POINTER(I64)])
+    sig("vlbm_batch_kernel_ms", I, [V, DP])
     sig("vlbm_batch_set_audit", I, [V, I])
     sig("vlbm_batch_audit", I, [V, C.POINTER(I64)])
     sig("vlbm_restrict_field", I, [I, I, DP, DP])
@@ -373,8 +374,11 @@ class BatchSimulation:
         mt, ma, ms = D(), D(), D()
         _check(lib().vlbm_batch_stats(self._h, C.byref(la), C.byref(mt), C.byref(ma),
                                       C.byref(ms), C.byref(cu)))
+        km = (D * 4)()
+        _check(lib().vlbm_batch_kernel_ms(self._h, km))
         return dict(launches=la.value, ms_theta=mt.value, ms_advance=ma.value,
-                    ms_sched=ms.value, cell_updates=cu.value)
+                    ms_sched=ms.value, cell_updates=cu.value, ms_theta_tiles=km[0],
+                    ms_theta_hard=km[1])
 
     def set_audit(self, on: bool = True) -> None:
         """Re-check every certified bisection step with the full feasible()."""

@@ -6,7 +6,7 @@ T=${1:-0.002}; TAG=${2:-x}
 mkdir -p gpurun_out
 VLBM_GROUPS=1 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'k_(theta|bisect|advance|sched)' \
   --nvtx --nvtx-include timed/ -c 180 --csv --log-file gpurun_out/kprof_$TAG.csv \
-  python bench.py --steps 40 --warmup 3 --t-start $T --no-cpu-baseline --no-postproc --no-e2e > /dev/null 2>&1
+  python bench.py --steps 40 --warmup 3 --t-start $T --no-cpu-baseline --no-postproc --no-e2e --no-roofline > /dev/null 2>&1
 python - "$TAG" <<'PY'
 import csv, sys, collections
 lines = open(f"gpurun_out/kprof_{sys.argv[1]}.csv").read().splitlines()

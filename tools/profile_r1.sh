@@ -1,0 +1,23 @@
+#!/bin/bash
+# Round-1 evidence on one B200 (run under gpurun from the repo root):
+#   1. the default bench line                       -> gpurun_out/r1_bench.json
+#   2. ncu launch list of the timed region           -> gpurun_out/r1_launches.csv
+#   3. ncu --set full of each march kernel at t=5e-4 (mid bench window, one
+#      sample group) and of the W1/L1 post-processing kernels (configs[3])
+#                                                    -> gpurun_out/r1_<kernel>.ncu-rep
+# tools/summarize_profiles.py turns these into profiles/r1_*.
+mkdir -p gpurun_out
+python bench.py > gpurun_out/r1_bench.json 2> gpurun_out/r1_bench.err
+B="python bench.py --steps 40 --warmup 3 --no-cpu-baseline --no-postproc --no-e2e --no-roofline"
+ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include timed/ -c 600 \
+    --csv --log-file gpurun_out/r1_launches.csv $B > gpurun_out/r1_launches.log 2>&1
+for k in k_theta_tiled k_theta_hard k_bisect_cert k_bisect_unc k_advance_tiled k_sched; do
+  VLBM_GROUPS=1 ncu --set full --import-source on --clock-control none -k regex:"$k" --nvtx \
+      --nvtx-include timed/ -c 1 -o gpurun_out/r1_$k -f $B --t-start 0.0005 \
+      > gpurun_out/r1_ncu_$k.log 2>&1
+done
+for k in k_w1_tile k_ordered_mean k_strong_partials; do
+  ncu --set full --import-source on --clock-control none -k regex:"$k" -s 1 -c 1 \
+      -o gpurun_out/r1_$k -f python tools/post_probe.py 1000 > gpurun_out/r1_ncu_$k.log 2>&1
+done
+ls -la gpurun_out/r1_*
