@@ -102,10 +102,11 @@ class ClockSampler:
 
 
 def fp64_profile():
-    """FP64 thread instructions per cell of the limiter kernels, from the
-    committed ncu capture (profiles/r1_fp64.json, made by tools/profile_r1.sh)."""
+    """Per-launch DRAM bytes of the advance and limiter kernels and the
+    limiter's FP64 instructions per cell, from the committed ncu capture
+    (profiles/r1_roofline_inputs.json: tools/profile_r1.sh + summarize_profiles.py)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r1_fp64.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r1_roofline_inputs.json")) as f:
             return json.load(f)
     except Exception:
         return None
@@ -376,25 +377,32 @@ def main():
         step_gbs = BYTES_PER_UPDATE * (updates / (ms * 1e-3)) / 1e9
         roof, fp64 = None, None
         if kern:
+            prof = fp64_profile() or {}
+            # The collide+stream kernel (BASELINE north_star: "roofline = bytes
+            # moved per cell update / HBM BW"): 320 B algorithmic per cell.
+            t_adv = kern["ms_advance"] * 1e-3
+            adv_gbs = BYTES_PER_UPDATE * cells_per_launch / t_adv / 1e9
+            roof = {"bound": "hbm", "kernel": "k_advance_tiled (collide+stream)",
+                    "achieved": adv_gbs, "peak": hbm, "unit": "GB/s", "frac": adv_gbs / hbm,
+                    "traffic": prof.get("k_advance_tiled_dram_bytes_per_launch"),
+                    "peak_source": src, "bytes_per_cell": BYTES_PER_UPDATE,
+                    "cells_per_launch": cells_per_launch, "launch_ms": kern["ms_advance"],
+                    "note": "per-launch times from a one-sample-group pass over the same step "
+                            "window; traffic from profiles/r1_kernels.csv (ncu --set full)"}
+            # The limiter's tile pass, the longest kernel of the step: FP64-bound.
             t_tiles = kern["ms_theta_tiles"] * 1e-3
-            achieved = THETA_BYTES_PER_CELL * cells_per_launch / t_tiles / 1e9
-            roof = {"bound": "hbm", "kernel": "k_theta_tiled", "achieved": achieved, "peak": hbm,
-                    "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
-                    "peak_source": src, "bytes_per_cell": THETA_BYTES_PER_CELL,
+            lim_gbs = THETA_BYTES_PER_CELL * cells_per_launch / t_tiles / 1e9
+            ops = prof.get("k_theta_tiled_fp64_inst_per_cell")
+            fp64 = {"kernel": "k_theta_tiled (RLMP limiter tile pass)",
                     "launch_ms": kern["ms_theta_tiles"],
-                    "note": "dominant kernel is FP64-bound, see fp64_roofline; per-launch "
-                            "times from a one-group pass over the same step window"}
-            prof = fp64_profile()
-            if prof:
-                roof["traffic"] = prof.get("k_theta_tiled_dram_bytes_per_launch")
-                ops = prof["k_theta_tiled_fp64_inst_per_cell"]
-                fp64 = {"kernel": "k_theta_tiled", "achieved": ops * cells_per_launch / t_tiles
-                        / 1e12, "peak": FP64_PEAK_TINST, "unit": "Tinst/s",
-                        "frac": ops * cells_per_launch / t_tiles / 1e12 / FP64_PEAK_TINST,
-                        "fp64_inst_per_cell": ops, "source": prof.get("source")}
-            adv_gbs = BYTES_PER_UPDATE * cells_per_launch / (kern["ms_advance"] * 1e-3) / 1e9
-            kern["advance_hbm"] = {"achieved": adv_gbs, "peak": hbm, "unit": "GB/s",
-                                   "frac": adv_gbs / hbm, "bytes_per_cell": BYTES_PER_UPDATE}
+                    "hbm": {"achieved": lim_gbs, "peak": hbm, "unit": "GB/s",
+                            "frac": lim_gbs / hbm, "bytes_per_cell": THETA_BYTES_PER_CELL,
+                            "traffic": prof.get("k_theta_tiled_dram_bytes_per_launch")},
+                    "source": prof.get("source")}
+            if ops:
+                rate = ops * cells_per_launch / t_tiles / 1e12
+                fp64.update({"achieved": rate, "peak": FP64_PEAK_TINST, "unit": "Tinst/s",
+                             "frac": rate / FP64_PEAK_TINST, "fp64_inst_per_cell": ops})
         line = {
             "metric": "VLBM sample-cell updates/s (GLUPS) & % HBM roofline; W1 post-proc cells/s",
             "value": value, "unit": "sample-cell-updates/s", "n_gpus": ws,
@@ -408,7 +416,7 @@ def main():
             "glups": value / 1e9,
             "gpu_launches": launches,
             "roofline": roof,
-            "fp64_roofline": fp64,
+            "limiter_roofline": fp64,
             "step_roofline": {"achieved": step_gbs, "peak": hbm, "unit": "GB/s",
                               "frac": step_gbs / hbm, "bytes_per_update": BYTES_PER_UPDATE},
             "kernel_ms_per_step": {"k_theta": theta_ms, "k_advance": adv_ms, "k_sched": sched_ms,

@@ -6,8 +6,9 @@ profiles/ (tracked):
                                     timed region (ncu launch list, serialised)
   profiles/<tag>_launches.csv       the launch list itself (ncu --csv)
   profiles/<tag>_ncu_details_<k>.csv  ncu --page details of each kernel
-  profiles/<tag>_fp64.json          FP64 instructions / DRAM bytes per launch of
-                                    the limiter tile pass (read by bench.py)
+  profiles/<tag>_roofline_inputs.json  DRAM bytes per launch of the advance and
+                                    limiter tile pass, limiter FP64 inst per cell
+                                    (read by bench.py)
 
 usage: python tools/summarize_profiles.py [tag] [gpurun_out]
 """
@@ -116,14 +117,17 @@ def main():
             w.writeheader()
             w.writerows(rows)
     share = launch_share()
-    tt = next((r for r in rows if r["kernel"] == "k_theta_tiled"), None)
-    if tt:
+    by = {r["kernel"]: r for r in rows}
+    if "k_theta_tiled" in by and "k_advance_tiled" in by:
+        tt, adv = by["k_theta_tiled"], by["k_advance_tiled"]
         fp = {"k_theta_tiled_fp64_inst_per_cell": tt["fp64_inst_per_item"],
               "k_theta_tiled_dram_bytes_per_launch": round(1e9 * (tt["dram_read_GB"]
                                                                   + tt["dram_write_GB"])),
+              "k_advance_tiled_dram_bytes_per_launch": round(1e9 * (adv["dram_read_GB"]
+                                                                    + adv["dram_write_GB"])),
               "source": f"profiles/{TAG}_kernels.csv (ncu --set full, C2 64 samples at t=5e-4, "
                         "one sample group)"}
-        with open(os.path.join(OUT, f"{TAG}_fp64.json"), "w") as f:
+        with open(os.path.join(OUT, f"{TAG}_roofline_inputs.json"), "w") as f:
             json.dump(fp, f, indent=1)
     for r in rows:
         print(r)
