@@ -148,37 +148,64 @@ __device__ __forceinline__ double dval(unsigned long long k) {
   return __longlong_as_double((long long)b);
 }
 
-// Bitonic sort of N = 32*R keys held by one warp, element e = lane*R + r.
+// Bitonic sort of N = 32*R keys held by one warp, every comparator ascending:
+// each merge size k starts with the "flip" step (partner e ^ (k-1), the
+// mirror image in the k-block) and continues with half-cleaners (partner
+// e ^ j); the lower index always takes the min.  No per-element direction logic: 3 instructions per element for an
+// in-register stage, 7 for a cross-lane one (2 shuffles, 64-bit compare, xor,
+// 2 selects).  Element e = lane*R + r.
 template <int R>
-__device__ __forceinline__ void warp_bitonic_sort(unsigned long long (&v)[R], int lane) {
+__device__ __forceinline__ void warp_sort_asc(unsigned long long (&v)[R], int lane) {
+  auto cas = [](unsigned long long& lo, unsigned long long& hi) {
+    const bool lt = hi < lo;
+    const unsigned long long a = lo, b = hi;
+    lo = lt ? b : a;
+    hi = lt ? a : b;
+  };
+  // cross-lane step: partner lane ^ m, partner register pr(r); this lane is the
+  // upper side iff (lane & topbit) != 0
+  auto xlane = [&](int m, int topbit, bool reverse) {
+    const bool upper = (lane & topbit) != 0;
+    auto upd = [&](unsigned long long& x, unsigned long long o) {
+      x = ((o < x) != upper) ? o : x;  // lower: min, upper: max
+    };
+    if (reverse) {  // partner register R-1-r: exchange mirrored pairs together
+#pragma unroll
+      for (int r = 0; r < (R + 1) / 2; ++r) {
+        const int q = R - 1 - r;
+        const unsigned long long o1 = __shfl_xor_sync(kFull, v[q], m);
+        if (q != r) {
+          const unsigned long long o2 = __shfl_xor_sync(kFull, v[r], m);
+          upd(v[q], o2);
+        }
+        upd(v[r], o1);
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) upd(v[r], __shfl_xor_sync(kFull, v[r], m));
+    }
+  };
 #pragma unroll
   for (int k = 2; k <= 32 * R; k <<= 1) {
+    // flip step
+    if (k <= R) {
 #pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int r = 0; r < R; ++r) {
+        const int r2 = r ^ (k - 1);
+        if (r < r2) cas(v[r], v[r2]);
+      }
+    } else {
+      xlane(k / R - 1, k / (2 * R), true);
+    }
+    // half-cleaners
+#pragma unroll
+    for (int j = k >> 2; j > 0; j >>= 1) {
       if (j >= R) {
-        const int lm = j / R;
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const unsigned long long o = __shfl_xor_sync(kFull, v[r], lm);
-          const int e = lane * R + r;
-          const bool take_min = (((e & j) == 0) == ((e & k) == 0));
-          const unsigned long long mn = o < v[r] ? o : v[r];
-          const unsigned long long mx = o < v[r] ? v[r] : o;
-          v[r] = take_min ? mn : mx;
-        }
+        xlane(j / R, j / R, false);
       } else {
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-          if ((r & j) == 0) {
-            const int r2 = r | j;
-            const int e = lane * R + r;
-            const bool asc = (e & k) == 0;
-            const unsigned long long x = v[r], y = v[r2];
-            const bool sw = asc ? (y < x) : (x < y);
-            v[r] = sw ? y : x;
-            v[r2] = sw ? x : y;
-          }
-        }
+        for (int r = 0; r < R; ++r)
+          if ((r & j) == 0) cas(v[r], v[r | j]);
       }
     }
   }
@@ -204,7 +231,7 @@ __device__ __forceinline__ double w1_cell(int M, int lane, double* ca, const dou
       const int m = r * 32 + lane;  // load slot order is free: sorting is order-free
       k[r] = m < M ? dkey(col[m]) : ~0ull;
     }
-    warp_bitonic_sort<R>(k, lane);
+    warp_sort_asc<R>(k, lane);
     if (pass == 0) {
       __syncwarp();
 #pragma unroll
@@ -292,7 +319,7 @@ __global__ void __launch_bounds__(32 * kW1Cells, 4) k_w1_tile(int M, long long n
 constexpr int kOmChunk = 2048;
 __global__ void __launch_bounds__(256) k_ordered_mean(long long n, const double* terms,
                                                      double* result) {
-  __shared__ double buf[2][kOmChunk];
+  __shared__ __align__(16) double buf[2][kOmChunk];
   const long long nchunks = (n + kOmChunk - 1) / kOmChunk;
   auto stage = [&](long long ch, int bi, int t0, int nt) {
     const long long c0 = ch * kOmChunk;
@@ -309,7 +336,29 @@ __global__ void __launch_bounds__(256) k_ordered_mean(long long n, const double*
     } else if (threadIdx.x == 0) {
       const long long c0 = ch * kOmChunk;
       const int nc = (int)((n - c0) < kOmChunk ? (n - c0) : kOmChunk);
-      for (int q = 0; q < nc; ++q) acc += buf[bi][q];
+      if (nc == kOmChunk) {
+        // software-pipelined: 16 values in registers while the next 16 load;
+        // the adds stay one dependent chain in storage order
+        const double2* b2 = reinterpret_cast<const double2*>(buf[bi]);
+        double2 x[8], y[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = b2[i];
+        for (int base = 0; base < kOmChunk / 2; base += 8) {
+          if (base + 8 < kOmChunk / 2) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) y[i] = b2[base + 8 + i];
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            acc += x[i].x;
+            acc += x[i].y;
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) x[i] = y[i];
+        }
+      } else {
+        for (int q = 0; q < nc; ++q) acc += buf[bi][q];
+      }
     }
     __syncthreads();
   }
@@ -389,23 +438,25 @@ static cudaError_t launch_w1(int M, long long n, int nxc, const double* a, long 
                              const double* b, long long bs, double* terms, cudaStream_t st) {
   if (M < 1 || M > 1024) return cudaErrorInvalidValue;
   const int grid = (int)((n + kW1Cells - 1) / kW1Cells);
-  auto go = [&](auto kernel, int R) {
-    const size_t smem = sizeof(double) * 2 * kW1Cells * (32 * R + 1);
+  auto go = [&](auto kernel, int R, int nbuf) {
+    const size_t smem = sizeof(double) * nbuf * kW1Cells * (32 * R + 1);
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kernel<<<grid, 32 * kW1Cells, smem, st>>>(M, n, nxc, a, as, b, bs, terms);
   };
+#define VLBM_W1_K(R) go(k_w1_tile<R, kKind>, R, 2)
   if (M <= 32)
-    go(k_w1_tile<1, kKind>, 1);
+    VLBM_W1_K(1);
   else if (M <= 64)
-    go(k_w1_tile<2, kKind>, 2);
+    VLBM_W1_K(2);
   else if (M <= 128)
-    go(k_w1_tile<4, kKind>, 4);
+    VLBM_W1_K(4);
   else if (M <= 256)
-    go(k_w1_tile<8, kKind>, 8);
+    VLBM_W1_K(8);
   else if (M <= 512)
-    go(k_w1_tile<16, kKind>, 16);
+    VLBM_W1_K(16);
   else
-    go(k_w1_tile<32, kKind>, 32);
+    VLBM_W1_K(32);
+#undef VLBM_W1_K
   return cudaGetLastError();
 }
 
