@@ -61,9 +61,9 @@ __global__ void k_restrict_var(int M, int nxc, int nyc, const double* fine, int 
 
 // ---------------------------------------------------------------------------
 // strong_error partials.  One CTA per sample; warps 1..3 stage (|a-b|, |b|)
-// for a chunk of cells into shared memory (double-buffered) while thread 0
-// runs the serial accumulation of the previous chunk in (cell, component)
-// order, exactly as metrics.hpp:71-80.
+// for a chunk of cells into shared memory (double-buffered) while warp 0
+// runs the serial accumulations of the previous chunk in (cell, component)
+// order, exactly as metrics.hpp:71-80, one sum per lane.
 constexpr int kSpChunk = 256;  // cells per chunk
 
 // Addressing: a(m, k, c) = a[m*as + k*ac + c]; b likewise with (bs, bc), or
@@ -77,62 +77,84 @@ __global__ void __launch_bounds__(128) k_strong_partials(int M, long long n, int
                                                          long long ac, const double* b,
                                                          long long bs, long long bc,
                                                          double* partials) {
-  __shared__ double sd[2][kSpChunk * kNC];
-  __shared__ double sr[2][kSpChunk * kNC];
+  __shared__ __align__(16) double sd[2][kSpChunk * kNC];
+  __shared__ __align__(16) double sr[2][kSpChunk * kNC];
   const int m = blockIdx.x;
   const double* A = a + (long long)m * as;
   const double* B = b + (long long)m * bs;
   const long long nchunks = (n + kSpChunk - 1) / kSpChunk;
+  // Staging: each thread issues the loads of all its items of the chunk
+  // before any shared store (kU items per loader thread), so a CTA keeps
+  // ~kU * 5 loads in flight per thread.
+  constexpr int kLoaders = 96, kU = (kSpChunk * kNC + kLoaders - 1) / kLoaders;
   auto stage = [&](long long ch, int buf, int t0, int nt) {
     const long long c0 = ch * kSpChunk;
-    for (int q = t0; q < kSpChunk * kNC; q += nt) {
+    double av[kU], bv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int q = t0 + u * nt;
       const int cl = q / kNC, k = q % kNC;
       const long long c = c0 + cl;
-      if (c < n) {
-        double bv;
+      av[u] = bv[u] = 0.0;
+      if (q < kSpChunk * kNC && c < n) {
         if (kFused) {
           const int j = (int)(c / nxc), i = (int)(c - (long long)j * nxc);
-          bv = restrict_at(B + (long long)k * bc, 2 * nxc, i, j);
+          bv[u] = restrict_at(B + (long long)k * bc, 2 * nxc, i, j);
         } else {
-          bv = B[(long long)k * bc + c];
+          bv[u] = B[(long long)k * bc + c];
         }
-        const double av = A[(long long)k * ac + c];
-        sd[buf][q] = fabs(av - bv);
-        sr[buf][q] = fabs(bv);
+        av[u] = A[(long long)k * ac + c];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int q = t0 + u * nt;
+      if (q < kSpChunk * kNC && c0 + q / kNC < n) {
+        sd[buf][q] = fabs(av[u] - bv[u]);
+        sr[buf][q] = fabs(bv[u]);
       }
     }
   };
-  stage(0, 0, threadIdx.x, blockDim.x);
+  // the first chunk is staged by the loader warps too (nt must be kLoaders)
+  if (threadIdx.x >= 32) stage(0, 0, threadIdx.x - 32, blockDim.x - 32);
   __syncthreads();
-  double num = 0.0, den = 0.0;
-  double cnum[4] = {0.0, 0.0, 0.0, 0.0}, cden[4] = {0.0, 0.0, 0.0, 0.0};
+  constexpr int kChains = kNC == 1 ? 2 : 2 + 2 * kNC;
+  static_assert(kNC == 1 || kNC == 4, "partials layout: num, den, cnum[4], cden[4]");
+  double acc = 0.0;
   for (long long ch = 0; ch < nchunks; ++ch) {
     const int buf = (int)(ch & 1);
     if (threadIdx.x >= 32) {
       if (ch + 1 < nchunks) stage(ch + 1, buf ^ 1, threadIdx.x - 32, blockDim.x - 32);
-    } else if (threadIdx.x == 0) {
+    } else if (threadIdx.x < kChains) {
+      // warp 0, lane l runs chain l: 0 num (every d), 1 den (every r), and
+      // with kNC > 1: 2+k cnum[k] (d of component k), 2+kNC+k cden[k].  The
+      // lanes issue the same instructions, so one (predicated) DADD per
+      // (cell, component) advances every chain in its own order.
+      const int l = threadIdx.x;
+      const double* src = (l == 0 || (l >= 2 && l < 2 + kNC)) ? sd[buf] : sr[buf];
+      const int kk = l < 2 ? -1 : (l - 2) % kNC;
       const long long c0 = ch * kSpChunk;
       const int nc = (int)((n - c0) < kSpChunk ? (n - c0) : kSpChunk);
       for (int cl = 0; cl < nc; ++cl) {
 #pragma unroll
         for (int k = 0; k < kNC; ++k) {
-          const double d = sd[buf][cl * kNC + k], r = sr[buf][cl * kNC + k];
-          num += d;
-          den += r;
-          cnum[k] += d;
-          cden[k] += r;
+          const double v = src[cl * kNC + k];
+          if (kk < 0 || kk == k) acc += v;
         }
       }
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < kChains) {
     double* o = partials + (long long)m * 10;
-    o[0] = num;
-    o[1] = den;
-    for (int k = 0; k < 4; ++k) {
-      o[2 + k] = cnum[k];
-      o[6 + k] = cden[k];
+    const int l = threadIdx.x;
+    if (kNC == 1) {  // one component: cnum[0] / cden[0] repeat num / den exactly
+      o[l] = acc;
+      o[l == 0 ? 2 : 6] = acc;
+      if (l == 0)
+        for (int k = 1; k < 4; ++k) o[2 + k] = o[6 + k] = 0.0;
+    } else {
+      o[l] = acc;  // 0 num, 1 den, 2..5 cnum, 6..9 cden
     }
   }
 }
@@ -151,9 +173,10 @@ __device__ __forceinline__ double dval(unsigned long long k) {
 // Bitonic sort of N = 32*R keys held by one warp, every comparator ascending:
 // each merge size k starts with the "flip" step (partner e ^ (k-1), the
 // mirror image in the k-block) and continues with half-cleaners (partner
-// e ^ j); the lower index always takes the min.  No per-element direction logic: 3 instructions per element for an
-// in-register stage, 7 for a cross-lane one (2 shuffles, 64-bit compare, xor,
-// 2 selects).  Element e = lane*R + r.
+// e ^ j); the lower index always takes the min.  No per-element direction
+// logic: 3 instructions per element for an in-register stage, 7 for a
+// cross-lane one (2 shuffles, 64-bit compare, xor, 2 selects).  Element
+// e = lane*R + r.
 template <int R>
 __device__ __forceinline__ void warp_sort_asc(unsigned long long (&v)[R], int lane) {
   auto cas = [](unsigned long long& lo, unsigned long long& hi) {
