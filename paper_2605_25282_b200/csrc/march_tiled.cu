@@ -95,43 +95,45 @@ __device__ __forceinline__ void tma_load_4d(double* dst, const CUtensorMap* map,
 __device__ __forceinline__ int clampi(int v, int lo, int hi) {
   return v < lo ? lo : (v > hi ? hi : v);
 }
-__device__ __forceinline__ double comp(const cs& v, int c) {
-  return c == 0 ? v.r : (c == 1 ? v.mx : (c == 2 ? v.my : v.e));
-}
 __device__ __forceinline__ bool in_domain(const MarchParams& P, int i, int j) {
   return i >= 0 && i < P.nx && j >= 0 && j < P.ny;
 }
 
-// Ghost value of plane `pl` (0..3: u, 4+4k+c: population k component c) at
-// padded (gi, gj): fill_ghosts semantics (solver.hpp:230-286).
-__device__ __forceinline__ double ghost_value(const MarchParams& P, const double* src,
-                                              const double* rows, int pl, int gi, int gj,
-                                              double inv2a) {
-  const Src r = resolve(P, clampi(gi, -2, P.nx + 1), clampi(gj, -2, P.ny + 1));
-  const int c = pl < 4 ? pl : (pl - 4) & 3;
-  const bool neg = r.mirror && c == 2;
-  double v;
-  if (pl < 4) {
-    v = r.inlet ? rows[4 * r.j + c] : src[c * P.plane + (long long)r.j * P.pitch + r.i];
-  } else {
-    const int k = (pl - 4) >> 2;
-    const int ks = r.mirror ? (k ^ ((k >> 1) & 1)) : k;  // {0,1,3,2} under the wall mirror
-    v = r.inlet ? comp(maxw_k(inlet_row(rows, r.j), ks, P.w, inv2a, P.gm1), c)
-                : src[(4 + 4 * ks + c) * P.plane + (long long)r.j * P.pitch + r.i];
-  }
-  return neg ? -v : v;
-}
-
 // Overwrite the out-of-domain cells of a staged box [planes][RY][RX] whose
-// cell (0, 0) is padded (bx, by) with their ghost values.
+// cell (0, 0) is padded (bx, by) with the ghost values of fill_ghosts
+// (solver.hpp:230-286): the ghost source is resolved once per cell, then
+// kPops = false fills the 4 u planes, kPops = true the 16 population planes
+// (population k of a wall ghost comes from k' = {0,1,3,2}[k], mom_y negated;
+// an inlet ghost holds u_in(row) and M_k(u_in, a)).
+template <bool kPops>
 __device__ __forceinline__ void patch_box(const MarchParams& P, const double* src,
                                           const double* rows, double* box, int RX, int RY, int bx,
-                                          int by, int pl0, int npl, double inv2a) {
+                                          int by, double inv2a) {
   const int n = RX * RY;
-  for (int e = threadIdx.x; e < n * npl; e += blockDim.x) {
-    const int q = e % n, pl = e / n;
+  auto put = [&](int k, int q, cs v, bool mirror) {
+    if (mirror) v.my = -v.my;
+    box[(4 * k) * n + q] = v.r;
+    box[(4 * k + 1) * n + q] = v.mx;
+    box[(4 * k + 2) * n + q] = v.my;
+    box[(4 * k + 3) * n + q] = v.e;
+  };
+  for (int q = threadIdx.x; q < n; q += blockDim.x) {
     const int gi = bx + q % RX, gj = by + q / RX;
-    if (!in_domain(P, gi, gj)) box[e] = ghost_value(P, src, rows, pl0 + pl, gi, gj, inv2a);
+    if (in_domain(P, gi, gj)) continue;
+    const Src r = resolve(P, clampi(gi, -2, P.nx + 1), clampi(gj, -2, P.ny + 1));
+    const long long off = (long long)r.j * P.pitch + r.i;
+    if (!kPops) {
+      put(0, q, r.inlet ? inlet_row(rows, r.j) : load_plane4(src, P.plane, off), r.mirror);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int ks = r.mirror ? (k ^ ((k >> 1) & 1)) : k;
+        put(k, q,
+            r.inlet ? maxw_k(inlet_row(rows, r.j), ks, P.w, inv2a, P.gm1)
+                    : load_plane4(src + (4 + 4 * ks) * P.plane, P.plane, off),
+            r.mirror);
+      }
+    }
   }
 }
 
@@ -255,8 +257,8 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_THETA_MINB)
   }
   mbar_wait(&bar, 0);
   if (!(x0 >= 2 && x0 + TX + 2 <= P.nx && y0 >= 2 && y0 + TY + 2 <= P.ny)) {
-    patch_box(P, src, rows, R, RX2, RY2, x0 - 2, y0 - 2, 0, 4, inv2a);
-    if (!VLBM_THETA_GPOP) patch_box(P, src, rows, SP, AX, AY, x0 - 2, y0 - 1, 4, 16, inv2a);
+    patch_box<false>(P, src, rows, R, RX2, RY2, x0 - 2, y0 - 2, inv2a);
+    if (!VLBM_THETA_GPOP) patch_box<true>(P, src, rows, SP, AX, AY, x0 - 2, y0 - 1, inv2a);
     __syncthreads();
   }
   double* F = R + 4 * NR2;
@@ -588,7 +590,7 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_ADV_MINB)
   // every cell of the tile has its four neighbours inside the domain
   const bool interior = x0 >= 1 && x0 + TX + 1 <= P.nx && y0 >= 1 && y0 + TY + 1 <= P.ny;
   if (!(x0 >= 2 && x0 + TX + 2 <= P.nx && y0 >= 1 && y0 + TY + 1 <= P.ny)) {
-    patch_box(P, src, rows, R, AX, AY, x0 - 2, y0 - 1, 0, 4, inv2a);
+    patch_box<false>(P, src, rows, R, AX, AY, x0 - 2, y0 - 1, inv2a);
     __syncthreads();
   }
   for (int q = threadIdx.x; q < NA; q += NT) flux_cell(R, NA, F, NA, q, inv2a, gm1, false);
