@@ -1,6 +1,6 @@
 // march_tiled.cu — the production march kernels for sm_100a.
 //
-// A CTA owns a TX x TY tile of interior cells of one sample (blockIdx.y), one
+// A CTA owns a TX x TY tile of interior cells of one sample (blockIdx.z), one
 // thread per cell.  The tile's inputs arrive in shared memory by TMA
 // (cp.async.bulk.tensor, 4-D tensor maps over [sample][plane][y][x] of each
 // state buffer, completion on an mbarrier): ONE bulk copy of the 20 state
@@ -226,20 +226,20 @@ __device__ __forceinline__ void enqueue_hard(const MarchParams& P, bool hard, lo
 
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(tiled::NT, VLBM_THETA_MINB)
-    k_theta_tiled(MarchParams P, int tiles_x, const __grid_constant__ CUtensorMap tmu0,
+    k_theta_tiled(MarchParams P, const __grid_constant__ CUtensorMap tmu0,
                   const __grid_constant__ CUtensorMap tmu1, const __grid_constant__ CUtensorMap tmp0,
                   const __grid_constant__ CUtensorMap tmp1) {
   using namespace tiled;
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) unsigned long long bar;
   __shared__ int qn, qbase;
-  const int s = blockIdx.y;
+  const int s = blockIdx.z;
   const SampleCtl* c = P.ctl + s;
   if (!c->active) return;
   double* R = sm;                    // u [4][NR2] by TMA, then inv2a f/g, p: [9][NR2]
   double* RF = R + kStagedTheta * NR2;  // rfo[NF], pfo[NF]
   double* SP = sm + kThetaSP;        // populations [16][NA] by TMA
-  const int x0 = (blockIdx.x % tiles_x) * TX, y0 = (blockIdx.x / tiles_x) * TY;
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
   const int parity = c->parity;
   const double* src = state_src(P, s, parity);
   const double* rows = P.inlet + (long long)s * P.ny * 4;
@@ -306,7 +306,8 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_THETA_MINB)
   bool hard = false, need = false;
   // Certificate hint of this warp (warp-uniform), see MarchParams::cert_hint.
   unsigned char* hint =
-      P.cert_hint ? P.cert_hint + ((long long)s * gridDim.x + blockIdx.x) * 8 + (threadIdx.x >> 5)
+      P.cert_hint ? P.cert_hint + (((long long)s * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 8 +
+                        (threadIdx.x >> 5)
                   : nullptr;
   const int h0 = hint ? *hint : 3;
   const bool try_cert = P.cert1 && (h0 >= 2 || (c->steps % kCertProbe) == 0);
@@ -562,18 +563,18 @@ __global__ void __launch_bounds__(256, 2) k_bisect_unc(MarchParams P) {
 // ---------------------------------------------------------------------------
 template <int kMode>
 __global__ void __launch_bounds__(tiled::NT, VLBM_ADV_MINB)
-    k_advance_tiled(MarchParams P, double const_theta, int tiles_x,
+    k_advance_tiled(MarchParams P, double const_theta,
                     const __grid_constant__ CUtensorMap tma0,
                     const __grid_constant__ CUtensorMap tma1) {
   using namespace tiled;
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) unsigned long long bar;
-  const int s = blockIdx.y;
+  const int s = blockIdx.z;
   SampleCtl* c = P.ctl + s;
   if (!c->active) return;
   double* R = sm;          // [4][NA]: u (TMA)
   double* F = sm + kAdvF;  // [8][NA]: inv2a f, inv2a g
-  const int x0 = (blockIdx.x % tiles_x) * TX, y0 = (blockIdx.x / tiles_x) * TY;
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
   const int parity = c->parity;
   const double* src = state_src(P, s, parity);
   double* dst = state_dst(P, s, parity);
@@ -688,10 +689,9 @@ static cudaError_t smem_attrs() {
 }
 
 static_assert(tiled::TX == 32 && tiled::TY == 8 && tiled::NT == 256, "theta_tiles() layout");
-static dim3 tiled_grid(const MarchParams& P, int& tiles_x) {
-  tiles_x = (P.nx + tiled::TX - 1) / tiled::TX;
-  const int ty = (P.ny + tiled::TY - 1) / tiled::TY;
-  return dim3(tiles_x * ty, P.S);
+// grid: (tile x, tile y, sample)
+static dim3 tiled_grid(const MarchParams& P) {
+  return dim3((P.nx + tiled::TX - 1) / tiled::TX, (P.ny + tiled::TY - 1) / tiled::TY, P.S);
 }
 
 // 4-D tensor maps [x = nx, y = ny, plane = 20, sample = S] over both state
@@ -740,9 +740,8 @@ int encode_tensor_maps(MarchParams& P) {
 
 cudaError_t launch_theta_tiled(const MarchParams& P, cudaStream_t st) {
   if (cudaError_t e = smem_attrs()) return e;
-  int tx;
-  const dim3 g = tiled_grid(P, tx);
-  k_theta_tiled<<<g, tiled::NT, tiled::kThetaSmem, st>>>(P, tx, P.tm_thu[0], P.tm_thu[1],
+  const dim3 g = tiled_grid(P);
+  k_theta_tiled<<<g, tiled::NT, tiled::kThetaSmem, st>>>(P, P.tm_thu[0], P.tm_thu[1],
                                                           P.tm_thp[0], P.tm_thp[1]);
   return cudaGetLastError();
 }
@@ -759,15 +758,14 @@ cudaError_t launch_theta_hard(const MarchParams& P, cudaStream_t st) {
 cudaError_t launch_advance_tiled(const MarchParams& P, int mode, double const_theta,
                                  cudaStream_t st) {
   if (cudaError_t e = smem_attrs()) return e;
-  int tx;
-  const dim3 g = tiled_grid(P, tx);
+  const dim3 g = tiled_grid(P);
   const size_t sm = tiled::kAdvanceSmem;
   if (mode == 0)
-    k_advance_tiled<0><<<g, tiled::NT, sm, st>>>(P, const_theta, tx, P.tm_adv[0], P.tm_adv[1]);
+    k_advance_tiled<0><<<g, tiled::NT, sm, st>>>(P, const_theta, P.tm_adv[0], P.tm_adv[1]);
   else if (mode == 1)
-    k_advance_tiled<1><<<g, tiled::NT, sm, st>>>(P, const_theta, tx, P.tm_adv[0], P.tm_adv[1]);
+    k_advance_tiled<1><<<g, tiled::NT, sm, st>>>(P, const_theta, P.tm_adv[0], P.tm_adv[1]);
   else
-    k_advance_tiled<2><<<g, tiled::NT, sm, st>>>(P, const_theta, tx, P.tm_adv[0], P.tm_adv[1]);
+    k_advance_tiled<2><<<g, tiled::NT, sm, st>>>(P, const_theta, P.tm_adv[0], P.tm_adv[1]);
   return cudaGetLastError();
 }
 
