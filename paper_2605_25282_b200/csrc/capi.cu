@@ -186,10 +186,13 @@ int alloc_batch(const vlbm_grid* g, const vlbm_params* p, int S, int device, vlb
   if (const char* e = getenv("VLBM_CERT1")) P.cert1 = atoi(e) != 0;
   {
     const size_t n = (size_t)S * vlbm_impl::theta_tiles(P.nx, P.ny) * 8;
+    if (n / 8 > (size_t)INT_MAX) rc = set_error(VLBM_E_INVALID, "too many tiles for one batch");
     chk(cudaMalloc(&P.cert_hint, n), "malloc cert_hint");
     if (rc == VLBM_OK) chk(cudaMemset(P.cert_hint, 3, n), "memset cert_hint");
   }
   int G = S >= 8 ? 2 : 1;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   if (const char* e = getenv("VLBM_GROUPS")) G = std::max(1, std::min(S, atoi(e)));
   b->G = G;
   chk(cudaMalloc(&b->d_active_g, sizeof(int) * G), "malloc active_g");
@@ -213,6 +216,7 @@ int alloc_batch(const vlbm_grid* g, const vlbm_params* p, int S, int device, vlb
     Q.inlet = P.inlet + (size_t)s0 * P.ny * 4;
     Q.n_active = b->d_active_g + g;
     Q.cert_hint = P.cert_hint + (size_t)s0 * vlbm_impl::theta_tiles(P.nx, P.ny) * 8;
+    Q.persist_ctas = std::max(1, sms * vlbm_impl::theta_ctas_per_sm() / G);
     cudaStream_t sg = b->stream;
     if (g > 0) chk(cudaStreamCreateWithFlags(&sg, cudaStreamNonBlocking), "stream g");
     if (p->limiter == VLBM_LIMITER_RLMP) {

@@ -78,6 +78,7 @@ struct MarchParams {
   // attempts; tried while >= 2, else re-probed every kCertProbe-th step.
   // k_theta_tiled's grid, 8 warps per tile; starts at 3.
   unsigned char* cert_hint;
+  int persist_ctas;  // grid of the persistent limiter tile pass (this group's share of the GPU)
   // TMA tensor maps [x, y, plane, sample] of buffer 0/1 with the tile boxes of
   // the advance (34x10x20), the limiter's u (36x12x4) and populations (34x10x16).
   CUtensorMap tm_adv[2], tm_thu[2], tm_thp[2];

@@ -225,6 +225,11 @@ __device__ __forceinline__ void enqueue_hard(const MarchParams& P, bool hard, lo
 }
 
 // ---------------------------------------------------------------------------
+// Persistent: each CTA walks the tiles t = blockIdx.x, +gridDim.x, ... of the
+// active samples (t = (sample * tiles_y + tile_y) * tiles_x + tile_x).  A
+// tile's staged data is read only until its cells hold u_FO, c_f and the
+// bounds in registers; then the CTA issues the NEXT tile's TMA into the same
+// buffers, so the load overlaps this tile's feasibility work.
 __global__ void __launch_bounds__(tiled::NT, VLBM_THETA_MINB)
     k_theta_tiled(MarchParams P, const __grid_constant__ CUtensorMap tmu0,
                   const __grid_constant__ CUtensorMap tmu1, const __grid_constant__ CUtensorMap tmp0,
@@ -233,159 +238,183 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_THETA_MINB)
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) unsigned long long bar;
   __shared__ int qn, qbase;
-  const int s = blockIdx.z;
-  const SampleCtl* c = P.ctl + s;
-  if (!c->active) return;
   double* R = sm;                    // u [4][NR2] by TMA, then inv2a f/g, p: [9][NR2]
   double* RF = R + kStagedTheta * NR2;  // rfo[NF], pfo[NF]
   double* SP = sm + kThetaSP;        // populations [16][NA] by TMA
-  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-  const int parity = c->parity;
-  const double* src = state_src(P, s, parity);
-  const double* rows = P.inlet + (long long)s * P.ny * 4;
-  const double inv2a = 0.5 / c->a;
+  const int tiles_x = (P.nx + TX - 1) / TX, tiles_y = (P.ny + TY - 1) / TY;
+  const int per_sample = tiles_x * tiles_y;
+  const int total = P.S * per_sample;  // < 2^31 tiles (host-checked)
   const double gm1 = P.gm1, w = P.w, al = P.alpha;
+  auto next_active = [&](int t) {
+    while (t < total && !P.ctl[t / per_sample].active) t += gridDim.x;
+    return t;
+  };
+  auto issue = [&](int t) {  // thread 0: the tile's TMA loads
+    const int s = t / per_sample, r = t - s * per_sample;
+    const int x0 = (r % tiles_x) * TX, y0 = (r / tiles_x) * TY;
+    const int parity = P.ctl[s].parity;
+    mbar_expect_tx(&bar, kThetaTx);
+    tma_load_4d(R, parity ? &tmu1 : &tmu0, &bar, x0 - 2, y0 - 2, 0, s);
+    if (!VLBM_THETA_GPOP) tma_load_4d(SP, parity ? &tmp1 : &tmp0, &bar, x0 - 2, y0 - 1, 4, s);
+  };
+  int t = next_active(blockIdx.x);
+  if (t >= total) return;
   if (threadIdx.x == 0) {
     qn = 0;
     mbar_init(&bar);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    mbar_expect_tx(&bar, kThetaTx);
-    tma_load_4d(R, parity ? &tmu1 : &tmu0, &bar, x0 - 2, y0 - 2, 0, s);
-    if (!VLBM_THETA_GPOP) tma_load_4d(SP, parity ? &tmp1 : &tmp0, &bar, x0 - 2, y0 - 1, 4, s);
-  }
-  mbar_wait(&bar, 0);
-  if (!(x0 >= 2 && x0 + TX + 2 <= P.nx && y0 >= 2 && y0 + TY + 2 <= P.ny)) {
-    patch_box<false>(P, src, rows, R, RX2, RY2, x0 - 2, y0 - 2, inv2a);
-    if (!VLBM_THETA_GPOP) patch_box<true>(P, src, rows, SP, AX, AY, x0 - 2, y0 - 1, inv2a);
+  if (threadIdx.x == 0) issue(t);
+  for (unsigned it = 0; t < total; ++it) {
+    const int s = t / per_sample, r = t - s * per_sample;
+    const int x0 = (r % tiles_x) * TX, y0 = (r / tiles_x) * TY;
+    const SampleCtl* c = P.ctl + s;
+    const int parity = c->parity;
+    const double* src = state_src(P, s, parity);
+    const double* rows = P.inlet + (long long)s * P.ny * 4;
+    const double inv2a = 0.5 / c->a;
+    mbar_wait(&bar, it & 1u);
+    if (!(x0 >= 2 && x0 + TX + 2 <= P.nx && y0 >= 2 && y0 + TY + 2 <= P.ny)) {
+      patch_box<false>(P, src, rows, R, RX2, RY2, x0 - 2, y0 - 2, inv2a);
+      if (!VLBM_THETA_GPOP) patch_box<true>(P, src, rows, SP, AX, AY, x0 - 2, y0 - 1, inv2a);
+      __syncthreads();
+    }
+    double* F = R + 4 * NR2;
+    for (int q = threadIdx.x; q < NR2; q += NT) flux_cell(R, NR2, F, NR2, q, inv2a, gm1, true);
     __syncthreads();
-  }
-  double* F = R + 4 * NR2;
-  for (int q = threadIdx.x; q < NR2; q += NT) flux_cell(R, NR2, F, NR2, q, inv2a, gm1, true);
-  __syncthreads();
 
-  // First-order candidates (compute_candidates, solver.hpp:301-316) on the
-  // tile and its 1-ring (the ring corners are never used).
-  auto rq = [](int x, int y) { return (y + 2) * RX2 + (x + 2); };
-  auto fq = [](int x, int y) { return (y + 1) * FX + (x + 1); };
-  auto M = [&](int q, int k) { return staged_m(R, NR2, F, NR2, q, k, w); };
-  auto ufo_at = [&](int x, int y) {
-    const cs a = add(M(rq(x - 1, y), 0), M(rq(x + 1, y), 1));
-    const cs b = add(M(rq(x, y - 1), 2), M(rq(x, y + 1), 3));
-    return add(add(a, b), scale(al, plane4(R, NR2, rq(x, y))));
-  };
-  const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
-  cs foC = ufo_at(tx, ty);
-  RF[fq(tx, ty)] = foC.r;
-  RF[NF + fq(tx, ty)] = pressure(foC, gm1);
-  if (threadIdx.x < 2 * TX + 2 * TY) {
-    const int t = threadIdx.x;
-    int x, y;
-    if (t < TX) {
-      x = t, y = -1;
-    } else if (t < 2 * TX) {
-      x = t - TX, y = TY;
-    } else if (t < 2 * TX + TY) {
-      x = -1, y = t - 2 * TX;
-    } else {
-      x = TX, y = t - 2 * TX - TY;
-    }
-    const cs fo = ufo_at(x, y);
-    RF[fq(x, y)] = fo.r;
-    RF[NF + fq(x, y)] = pressure(fo, gm1);
-  }
-  __syncthreads();
-
-  // Limiter inputs of this thread's cell (face_corrections :321-329,
-  // rlmp_bounds :364-435) and the theta = 1 test.
-  const int i = x0 + tx, j = y0 + ty;
-  const bool valid = i < P.nx && j < P.ny;
-  cs cf[4];
-  RlmpBounds b;
-  bool hard = false, need = false;
-  // Certificate hint of this warp (warp-uniform), see MarchParams::cert_hint.
-  unsigned char* hint =
-      P.cert_hint ? P.cert_hint + (((long long)s * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 8 +
-                        (threadIdx.x >> 5)
-                  : nullptr;
-  const int h0 = hint ? *hint : 3;
-  const bool try_cert = P.cert1 && (h0 >= 2 || (c->steps % kCertProbe) == 0);
-  if (valid) {
-    auto pop = [&](int k, int x, int y) {
-      if (VLBM_THETA_GPOP) {
-        const int ii = x0 + x, jj = y0 + y;
-        if (ii >= 0 && ii < P.nx && jj >= 0 && jj < P.ny)
-          return load_plane4(src + (4 + 4 * k) * P.plane, P.plane, (long long)jj * P.pitch + ii);
-        return load_pop(P, src, rows, k, ii, jj, inv2a);
-      }
-      return plane4(SP + 4 * k * NA, NA, (y + 1) * AX + (x + 2));
+    // First-order candidates (compute_candidates, solver.hpp:301-316) on the
+    // tile and its 1-ring (the ring corners are never used).
+    auto rq = [](int x, int y) { return (y + 2) * RX2 + (x + 2); };
+    auto fq = [](int x, int y) { return (y + 1) * FX + (x + 1); };
+    auto M = [&](int q, int k) { return staged_m(R, NR2, F, NR2, q, k, w); };
+    auto ufo_at = [&](int x, int y) {
+      const cs a = add(M(rq(x - 1, y), 0), M(rq(x + 1, y), 1));
+      const cs b = add(M(rq(x, y - 1), 2), M(rq(x, y + 1), 3));
+      return add(add(a, b), scale(al, plane4(R, NR2, rq(x, y))));
     };
-    const int qc = rq(tx, ty);
-    cf[0] = sub(sub(M(rq(tx - 1, ty), 0), pop(0, tx - 1, ty)), sub(M(qc, 1), pop(1, tx, ty)));
-    cf[1] = sub(sub(M(rq(tx + 1, ty), 1), pop(1, tx + 1, ty)), sub(M(qc, 0), pop(0, tx, ty)));
-    cf[2] = sub(sub(M(rq(tx, ty - 1), 2), pop(2, tx, ty - 1)), sub(M(qc, 3), pop(3, tx, ty)));
-    cf[3] = sub(sub(M(rq(tx, ty + 1), 3), pop(3, tx, ty + 1)), sub(M(qc, 2), pop(2, tx, ty)));
-    RlmpStencil st;
-    st.fo = foC;
-    const int fpts[5] = {fq(tx, ty), fq(tx - 1, ty), fq(tx + 1, ty), fq(tx, ty - 1), fq(tx, ty + 1)};
-#pragma unroll
-    for (int n = 0; n < 5; ++n) {
-      st.rfo[n] = RF[fpts[n]];
-      st.pfo[n] = RF[NF + fpts[n]];
-    }
-    const int rpts[9] = {rq(tx, ty),     rq(tx - 1, ty), rq(tx + 1, ty), rq(tx, ty - 1), rq(tx, ty + 1),
-                         rq(tx - 2, ty), rq(tx + 2, ty), rq(tx, ty - 2), rq(tx, ty + 2)};
-#pragma unroll
-    for (int n = 0; n < 9; ++n) {
-      st.rprev[n] = R[rpts[n]];
-      st.pprev[n] = F[8 * NR2 + rpts[n]];
-    }
-    b = rlmp_bounds(st, P.kappa, P.rho_floor_coef, P.p_floor_coef);
-    const cs delta = add(add(cf[0], cf[1]), add(cf[2], cf[3]));
-    // feasible(1): the diagonal first; the 15 vertex floors only when the
-    // certificate cannot prove them.
-    if (diag_ok(1.0, foC, delta, b, gm1)) {
-      double parts[2] = {0.0, 0.0};
-      const bool cert = try_cert && vertices_certified_at_one(foC, st.pfo[0], cf, b.rho_floor,
-                                                             b.p_floor, gm1,
-                                                             P.audit ? parts : nullptr);
-      need = !cert;
-      const bool ok = cert || vertex_floors_ok(1.0, foC, cf, b, gm1);
-      if (P.audit) {  // [8] diagonal passed, [9] certified, [10] feasible; [0] certificate errors
-        atomicAdd(P.audit + 8, 1);
-        if (cert) atomicAdd(P.audit + 9, 1);
-        if (ok) atomicAdd(P.audit + 10, 1);
-        if (cert && !vertex_floors_ok(1.0, foC, cf, b, gm1)) atomicAdd(P.audit, 1);
-        if (!cert && ok) {
-          // [12] uncertified but feasible; [13] of those the true vertex
-          // minimum is above p_FO / 2 (bound loose); [14] quadratic part
-          // dominates the bound
-          double pmin = st.pfo[0];
-          for (int mask = 1; mask < 16; ++mask)
-            pmin = smin(pmin, pressure(vertex_at(foC, cf, mask), gm1));
-          atomicAdd(P.audit + 12, 1);
-          if (pmin > 0.5 * st.pfo[0]) atomicAdd(P.audit + 13, 1);
-          if (parts[1] > parts[0]) atomicAdd(P.audit + 14, 1);
-        }
+    const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
+    cs foC = ufo_at(tx, ty);
+    RF[fq(tx, ty)] = foC.r;
+    RF[NF + fq(tx, ty)] = pressure(foC, gm1);
+    if (threadIdx.x < 2 * TX + 2 * TY) {
+      const int q = threadIdx.x;
+      int x, y;
+      if (q < TX) {
+        x = q, y = -1;
+      } else if (q < 2 * TX) {
+        x = q - TX, y = TY;
+      } else if (q < 2 * TX + TY) {
+        x = -1, y = q - 2 * TX;
+      } else {
+        x = TX, y = q - 2 * TX - TY;
       }
-      if (ok)
-        P.theta[(long long)s * P.plane + (long long)j * P.pitch + i] = 1.0;
-      else
+      const cs fo = ufo_at(x, y);
+      RF[fq(x, y)] = fo.r;
+      RF[NF + fq(x, y)] = pressure(fo, gm1);
+    }
+    __syncthreads();
+
+    // Limiter inputs of this thread's cell (face_corrections :321-329,
+    // rlmp_bounds :364-435): the last reads of the staged tile.
+    const int i = x0 + tx, j = y0 + ty;
+    const bool valid = i < P.nx && j < P.ny;
+    cs cf[4], delta;
+    RlmpBounds b;
+    double pfo0 = 0.0;
+    bool hard = false, need = false;
+    if (valid) {
+      auto pop = [&](int k, int x, int y) {
+        if (VLBM_THETA_GPOP) {
+          const int ii = x0 + x, jj = y0 + y;
+          if (ii >= 0 && ii < P.nx && jj >= 0 && jj < P.ny)
+            return load_plane4(src + (4 + 4 * k) * P.plane, P.plane, (long long)jj * P.pitch + ii);
+          return load_pop(P, src, rows, k, ii, jj, inv2a);
+        }
+        return plane4(SP + 4 * k * NA, NA, (y + 1) * AX + (x + 2));
+      };
+      const int qc = rq(tx, ty);
+      cf[0] = sub(sub(M(rq(tx - 1, ty), 0), pop(0, tx - 1, ty)), sub(M(qc, 1), pop(1, tx, ty)));
+      cf[1] = sub(sub(M(rq(tx + 1, ty), 1), pop(1, tx + 1, ty)), sub(M(qc, 0), pop(0, tx, ty)));
+      cf[2] = sub(sub(M(rq(tx, ty - 1), 2), pop(2, tx, ty - 1)), sub(M(qc, 3), pop(3, tx, ty)));
+      cf[3] = sub(sub(M(rq(tx, ty + 1), 3), pop(3, tx, ty + 1)), sub(M(qc, 2), pop(2, tx, ty)));
+      RlmpStencil st;
+      st.fo = foC;
+      const int fpts[5] = {fq(tx, ty), fq(tx - 1, ty), fq(tx + 1, ty), fq(tx, ty - 1),
+                           fq(tx, ty + 1)};
+#pragma unroll
+      for (int n = 0; n < 5; ++n) {
+        st.rfo[n] = RF[fpts[n]];
+        st.pfo[n] = RF[NF + fpts[n]];
+      }
+      const int rpts[9] = {rq(tx, ty),     rq(tx - 1, ty), rq(tx + 1, ty),
+                           rq(tx, ty - 1), rq(tx, ty + 1), rq(tx - 2, ty),
+                           rq(tx + 2, ty), rq(tx, ty - 2), rq(tx, ty + 2)};
+#pragma unroll
+      for (int n = 0; n < 9; ++n) {
+        st.rprev[n] = R[rpts[n]];
+        st.pprev[n] = F[8 * NR2 + rpts[n]];
+      }
+      b = rlmp_bounds(st, P.kappa, P.rho_floor_coef, P.p_floor_coef);
+      pfo0 = st.pfo[0];
+      delta = add(add(cf[0], cf[1]), add(cf[2], cf[3]));
+    }
+    // The staged buffers are free: prefetch the next tile.
+    const int tn = next_active(t + (int)gridDim.x);
+    __syncthreads();
+    if (threadIdx.x == 0 && tn < total) issue(tn);
+
+    // feasible(1): the diagonal first; the 15 vertex floors only when the
+    // certificate cannot prove them.  Certificate hint of this warp (warp-
+    // uniform), see MarchParams::cert_hint.
+    unsigned char* hint =
+        P.cert_hint ? P.cert_hint + (long long)t * 8 + (threadIdx.x >> 5) : nullptr;
+    const int h0 = hint ? *hint : 3;
+    const bool try_cert = P.cert1 && (h0 >= 2 || (c->steps % kCertProbe) == 0);
+    if (valid) {
+      if (diag_ok(1.0, foC, delta, b, gm1)) {
+        double parts[2] = {0.0, 0.0};
+        const bool cert = try_cert && vertices_certified_at_one(foC, pfo0, cf, b.rho_floor,
+                                                               b.p_floor, gm1,
+                                                               P.audit ? parts : nullptr);
+        need = !cert;
+        const bool ok = cert || vertex_floors_ok(1.0, foC, cf, b, gm1);
+        if (P.audit) {  // [8] diagonal passed, [9] certified, [10] feasible; [0] certificate errors
+          atomicAdd(P.audit + 8, 1);
+          if (cert) atomicAdd(P.audit + 9, 1);
+          if (ok) atomicAdd(P.audit + 10, 1);
+          if (cert && !vertex_floors_ok(1.0, foC, cf, b, gm1)) atomicAdd(P.audit, 1);
+          if (!cert && ok) {
+            // [12] uncertified but feasible; [13] of those the true vertex
+            // minimum is above p_FO / 2 (bound loose); [14] quadratic part
+            // dominates the bound
+            double pmin = pfo0;
+            for (int mask = 1; mask < 16; ++mask)
+              pmin = smin(pmin, pressure(vertex_at(foC, cf, mask), gm1));
+            atomicAdd(P.audit + 12, 1);
+            if (pmin > 0.5 * pfo0) atomicAdd(P.audit + 13, 1);
+            if (parts[1] > parts[0]) atomicAdd(P.audit + 14, 1);
+          }
+        }
+        if (ok)
+          P.theta[(long long)s * P.plane + (long long)j * P.pitch + i] = 1.0;
+        else
+          hard = true;
+      } else {
         hard = true;
-    } else {
-      hard = true;
+      }
     }
-  }
-  {
-    const unsigned m = __ballot_sync(0xffffffffu, need);
-    if ((threadIdx.x & 31) == 0) {
-      if (hint && try_cert) *hint = (unsigned char)(m == 0 ? min(h0 + 1, 3) : max(h0 - 1, 0));
-      if (P.audit && m) atomicAdd(P.audit + 11, 1);  // [11] warps with vertex checks left
+    {
+      const unsigned m = __ballot_sync(0xffffffffu, need);
+      if ((threadIdx.x & 31) == 0) {
+        if (hint && try_cert) *hint = (unsigned char)(m == 0 ? min(h0 + 1, 3) : max(h0 - 1, 0));
+        if (P.audit && m) atomicAdd(P.audit + 11, 1);  // [11] warps with vertex checks left
+      }
     }
+    const long long cell = (long long)s * P.plane + (long long)j * P.pitch + i;
+    enqueue_hard(P, hard, cell, foC, cf, b, gm1, qn, qbase);
+    t = tn;
   }
-  const long long cell = (long long)s * P.plane + (long long)j * P.pitch + i;
-  enqueue_hard(P, hard, cell, foC, cf, b, gm1, qn, qbase);
 }
 
 // The limiter's hard cells, in three convergent passes (the rest of
@@ -740,10 +769,21 @@ int encode_tensor_maps(MarchParams& P) {
 
 cudaError_t launch_theta_tiled(const MarchParams& P, cudaStream_t st) {
   if (cudaError_t e = smem_attrs()) return e;
-  const dim3 g = tiled_grid(P);
+  // persistent: the resident CTAs of this sample group's share of the GPU
+  const long long tiles = (long long)P.S * theta_tiles(P.nx, P.ny);
+  const int g = (int)(tiles < P.persist_ctas ? tiles : P.persist_ctas);
   k_theta_tiled<<<g, tiled::NT, tiled::kThetaSmem, st>>>(P, P.tm_thu[0], P.tm_thu[1],
                                                           P.tm_thp[0], P.tm_thp[1]);
   return cudaGetLastError();
+}
+
+int theta_ctas_per_sm() {
+  if (smem_attrs() != cudaSuccess) return 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_theta_tiled, tiled::NT,
+                                                    tiled::kThetaSmem) != cudaSuccess)
+    return 1;
+  return n > 0 ? n : 1;
 }
 
 cudaError_t launch_theta_hard(const MarchParams& P, cudaStream_t st) {
