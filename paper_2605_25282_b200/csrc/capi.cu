@@ -231,7 +231,7 @@ int alloc_batch(const vlbm_grid* g, const vlbm_params* p, int S, int device, vlb
         chk(cudaMalloc(&Q.bq_idx, sizeof(long long) * cap), "malloc bq_idx");
         chk(cudaMalloc(&Q.cq, sizeof(double) * vlbm_dev::kUncWords * cap), "malloc cq");
         chk(cudaMalloc(&Q.cq_idx, sizeof(long long) * cap), "malloc cq_idx");
-        // counters: [0] hard cells, [2] bq, [3..5] cq bins
+        // counters: [0] hard cells, [2] bq, [3..5] cq bins, [6] limiter tile claims
         chk(cudaMalloc(&Q.hq_n, 8 * sizeof(int)), "malloc hq_n");
         Q.hq_next = Q.hq_n + 1;
         if (rc == VLBM_OK) chk(cudaMemset(Q.hq_n, 0, 8 * sizeof(int)), "memset hq_n");

@@ -225,8 +225,9 @@ __device__ __forceinline__ void enqueue_hard(const MarchParams& P, bool hard, lo
 }
 
 // ---------------------------------------------------------------------------
-// Persistent: each CTA walks the tiles t = blockIdx.x, +gridDim.x, ... of the
-// active samples (t = (sample * tiles_y + tile_y) * tiles_x + tile_x).  A
+// Persistent: each CTA starts at tile blockIdx.x and then claims tiles from a
+// per-step counter, skipping inactive samples (t = (sample * tiles_y +
+// tile_y) * tiles_x + tile_x).  A
 // tile's staged data is read only until its cells hold u_FO, c_f and the
 // bounds in registers; then the CTA issues the NEXT tile's TMA into the same
 // buffers, so the load overlaps this tile's feasibility work.
@@ -237,7 +238,7 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_THETA_MINB)
   using namespace tiled;
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) unsigned long long bar;
-  __shared__ int qn, qbase;
+  __shared__ int qn, qbase, s_next;
   double* R = sm;                    // u [4][NR2] by TMA, then inv2a f/g, p: [9][NR2]
   double* RF = R + kStagedTheta * NR2;  // rfo[NF], pfo[NF]
   double* SP = sm + kThetaSP;        // populations [16][NA] by TMA
@@ -248,6 +249,17 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_THETA_MINB)
   auto next_active = [&](int t) {
     while (t < total && !P.ctl[t / per_sample].active) t += gridDim.x;
     return t;
+  };
+  // thread 0: the next tile of this CTA -- claimed from the step's tile
+  // counter (hq_n[6], reset by k_sched) so CTAs stay balanced whatever the
+  // per-tile cost (boundary tiles, hard cells); static striding without queues
+  auto claim = [&](int t) {
+    if (!P.hq_n) return next_active(t + (int)gridDim.x);
+    int tn;
+    do {
+      tn = (int)gridDim.x + atomicAdd(P.hq_n + 6, 1);
+    } while (tn < total && !P.ctl[tn / per_sample].active);
+    return tn;
   };
   auto issue = [&](int t) {  // thread 0: the tile's TMA loads
     const int s = t / per_sample, r = t - s * per_sample;
@@ -360,9 +372,12 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_THETA_MINB)
       delta = add(add(cf[0], cf[1]), add(cf[2], cf[3]));
     }
     // The staged buffers are free: prefetch the next tile.
-    const int tn = next_active(t + (int)gridDim.x);
     __syncthreads();
-    if (threadIdx.x == 0 && tn < total) issue(tn);
+    if (threadIdx.x == 0) {
+      const int tn = claim(t);
+      s_next = tn;
+      if (tn < total) issue(tn);
+    }
 
     // feasible(1): the diagonal first; the 15 vertex floors only when the
     // certificate cannot prove them.  Certificate hint of this warp (warp-
@@ -412,8 +427,8 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_THETA_MINB)
       }
     }
     const long long cell = (long long)s * P.plane + (long long)j * P.pitch + i;
-    enqueue_hard(P, hard, cell, foC, cf, b, gm1, qn, qbase);
-    t = tn;
+    enqueue_hard(P, hard, cell, foC, cf, b, gm1, qn, qbase);  // starts with __syncthreads
+    t = s_next;
   }
 }
 
