@@ -32,7 +32,7 @@ CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math"
 
 CU_SOURCES = ["march.cu", "march_tiled.cu", "post.cu", "capi.cu"]
 CPP_SOURCES = ["host_ic.cpp"]
-HEADERS = ["vlbm_device.cuh", "march.cuh", "march_common.cuh", "rlmp.cuh", "internal.h"]
+HEADERS = ["vlbm_device.cuh", "march.cuh", "march_common.cuh", "rlmp.cuh", "rlmp_replay.cuh", "internal.h"]
 
 
 def _newer(target: str, deps: list[str]) -> bool:

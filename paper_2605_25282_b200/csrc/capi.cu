@@ -184,6 +184,8 @@ int alloc_batch(const vlbm_grid* g, const vlbm_params* p, int S, int device, vlb
   // group's FP64-bound limiter.  VLBM_GROUPS overrides the default.
   P.cert1 = 1;
   if (const char* e = getenv("VLBM_CERT1")) P.cert1 = atoi(e) != 0;
+  P.replay = 1;
+  if (const char* e = getenv("VLBM_REPLAY")) P.replay = atoi(e) != 0;
   {
     const size_t n = (size_t)S * vlbm_impl::theta_tiles(P.nx, P.ny) * 8;
     if (n / 8 > (size_t)INT_MAX) rc = set_error(VLBM_E_INVALID, "too many tiles for one batch");
@@ -351,7 +353,7 @@ int march_loop(vlbm_batch* b, double target, double fixed_dt, int mode, int chun
         record(b, 2, st);
         CU(vlbm_impl::launch_advance(Q, adv_mode, const_theta, st));
         record_end(b);
-        b->launches += rlmp ? (Q.hq ? 6 : 3) : 2;
+        b->launches += rlmp ? (Q.hq ? (Q.replay ? 7 : 6) : 3) : 2;
       }
     }
     for (int g = 0; g < G; ++g)

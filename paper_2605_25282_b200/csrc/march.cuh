@@ -64,7 +64,9 @@ struct MarchParams {
   int* hq_next;  // unused slot (hq_n[1]); hq_n[2], hq_n[3]: bisection queue counts
   int hq_cap;
   // Bisection queues (capacity hq_cap each), filled by k_theta_hard:
-  //   bq: vertices all certified -- u_FO(4), delta(4), rho_lo/hi, p_lo/hi, thc  (kBisWords)
+  //   bq: vertices all certified -- u_FO(4), delta(4), rho_lo/hi, p_lo/hi, thc  (kBisWords);
+  //       after k_bisect_cert (replay on) it holds the bisections k_bisect_unc
+  //       stopped: lo, hi in words 0, 1; bq_idx = cq slot | step << 40 (count hq_n[7])
   //   cq: some uncertified -- u_FO(4), c_f(16), rho_lo/hi, p_lo/hi, thc, p0, err, er (kUncWords)
   //   *_idx: cell index; cq_idx packs the uncertified-vertex mask in bits 40..55
   double* bq;
@@ -73,6 +75,8 @@ struct MarchParams {
   long long* cq_idx;
   int* audit;    // optional: disagreements of the certified bisection (must stay 0)
   int cert1;     // use the theta = 1 vertex certificate (A/B switch VLBM_CERT1, default on)
+  int replay;    // k_bisect_unc replays its bisections from certified classifications
+                 // (rlmp_replay.cuh; A/B switch VLBM_REPLAY, default on)
   // Per (sample, tile, warp) hint of the limiter: a 2-bit saturating count of
   // the certificate proving every lane's vertex floors (+1) or not (-1) at its
   // attempts; tried while >= 2, else re-probed every kCertProbe-th step.

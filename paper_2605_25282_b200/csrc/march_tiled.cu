@@ -27,6 +27,7 @@
 #include "march.cuh"
 #include "march_common.cuh"
 #include "rlmp.cuh"
+#include "rlmp_replay.cuh"
 
 #ifndef VLBM_THETA_GPOP
 #define VLBM_THETA_GPOP 0  // 1: limiter reads populations from global (no SP stage)
@@ -220,7 +221,7 @@ __device__ __forceinline__ void enqueue_hard(const MarchParams& P, bool hard, lo
     P.hq_idx[qbase + slot] = cell;
   } else {  // queue full (or absent): finish in place
     if (P.hq && qbase + slot < P.hq_cap) P.hq_idx[qbase + slot] = -1;
-    P.theta[cell] = rlmp_theta_hard(fo, cf, b, gm1, P.audit);
+    P.theta[cell] = rlmp_theta_hard(fo, cf, b, gm1, P.audit);  // rare: plain bisection
   }
 }
 
@@ -439,7 +440,9 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_THETA_MINB)
 //                   vertex certificates; cells that must bisect go to bq (all
 //                   vertices certified) or cq (some not)
 //   k_bisect_cert   30 diagonal-only steps: every lane runs the same code
-//   k_bisect_unc    30 steps re-checking the uncertified vertices
+//   k_bisect_unc    30 steps re-checking the uncertified vertices (replay on:
+//                   the bisection replayed, rlmp_replay.cuh)
+//   k_bisect_tail   the replayed bisections that need more exact steps
 // Queues use block-aggregated slots (one global atomic per CTA pass); a CTA
 // that would overflow a queue finishes those cells in place.
 __device__ __forceinline__ void load_hard_entry(const MarchParams& P, int slot, cs& fo, cs* cf,
@@ -493,12 +496,12 @@ __global__ void __launch_bounds__(256, 2) k_theta_hard(MarchParams P) {
         if (h.done) {
           P.theta[idx] = h.result;
         } else {
-          cls = (h.unc || P.audit) ? 2 : 1;
-          ccls = unc_class(h.unc);
           if (P.audit) {
             atomicAdd(P.audit + 1, 1);
             atomicAdd(P.audit + (h.unc ? 3 : 2), 1);
           }
+          cls = (h.unc || P.audit) ? 2 : 1;
+          ccls = unc_class(h.unc);
         }
       }
     }
@@ -569,38 +572,106 @@ __global__ void __launch_bounds__(256) k_bisect_cert(MarchParams P) {
   }
 }
 
+// One cq entry (k_theta_hard's layout) back into registers.
+__device__ __forceinline__ void load_unc_entry(const MarchParams& P, int s, long long packed, cs& fo,
+                                               cs* cf, RlmpBounds& b, HardStage& h) {
+  const long long cap = P.hq_cap;
+  const double* q = P.cq + s;
+  fo = {q[0], q[cap], q[2 * cap], q[3 * cap]};
+#pragma unroll
+  for (int f = 0; f < 4; ++f)
+    cf[f] = {q[(4 + 4 * f) * cap], q[(5 + 4 * f) * cap], q[(6 + 4 * f) * cap],
+             q[(7 + 4 * f) * cap]};
+  b.rho_lo = q[20 * cap], b.rho_hi = q[21 * cap], b.p_lo = q[22 * cap], b.p_hi = q[23 * cap];
+  b.rho_floor = P.rho_floor_coef;
+  b.p_floor = P.p_floor_coef;
+  h.done = false;
+  h.thc = q[24 * cap];
+  h.p0 = q[25 * cap];
+  h.err = q[26 * cap];
+  h.certifiable = h.err >= 0.0;
+  h.er = q[27 * cap];
+  h.mhi = (unsigned)(packed >> 40) & kAllVertices;
+  h.lo_all = ((packed >> 56) & 1) != 0;
+  h.unc = kAllVertices & ~((h.lo_all ? kAllVertices : 0u) & h.mhi);
+}
+
+// Steps a replayed bisection may evaluate exactly in k_bisect_unc; a cell
+// that needs more (its classifications leave a wide band) continues in
+// k_bisect_tail, so no warp waits on one lane's long exact tail.
+constexpr int kReplayInline = 2;
+
 // blockIdx.y = cq bin; bins run concurrently.
-__global__ void __launch_bounds__(256, 2) k_bisect_unc(MarchParams P) {
+#ifndef VLBM_UNC_MINB
+#define VLBM_UNC_MINB 2
+#endif
+__global__ void __launch_bounds__(256, VLBM_UNC_MINB) k_bisect_unc(MarchParams P) {
+  __shared__ int nt, tbase;
   const int third = P.hq_cap / 3;
   const int n = min(P.hq_n[3 + blockIdx.y], third);
   const long long cap = P.hq_cap;
-  for (int s0 = blockIdx.x * blockDim.x + threadIdx.x; s0 < n; s0 += gridDim.x * blockDim.x) {
+  for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
+    const int s0 = base + threadIdx.x;
     const int s = (int)blockIdx.y * third + s0;
+    const long long packed = s0 < n ? P.cq_idx[s] : -1;
+    bool stopped = false;
+    Bracket br;
+    if (packed >= 0) {
+      cs fo, cf[4];
+      RlmpBounds b;
+      HardStage h;
+      load_unc_entry(P, s, packed, fo, cf, b, h);
+      const cs delta = add(add(cf[0], cf[1]), add(cf[2], cf[3]));
+      if (P.replay) {
+        stopped = !bisect_replay(fo, cf, delta, b, h, P.gm1, kReplayInline, br, P.audit);
+        if (!stopped) P.theta[packed & kIdxMask] = br.lo;
+      } else {
+        P.theta[packed & kIdxMask] = bisect_uncertified(fo, cf, delta, b, h, P.gm1, P.audit);
+      }
+    }
+    if (!P.replay) continue;  // uniform across the CTA
+    // stopped bisections -> the tail queue (bq storage; k_bisect_cert is done)
+    if (threadIdx.x == 0) nt = 0;
+    __syncthreads();
+    const int my = stopped ? atomicAdd(&nt, 1) : 0;
+    __syncthreads();
+    if (threadIdx.x == 0) tbase = nt ? atomicAdd(P.hq_n + 7, nt) : 0;
+    __syncthreads();
+    if (stopped) {
+      const int t = tbase + my;
+      if (tbase + nt <= P.hq_cap) {
+        P.bq[t] = br.lo;
+        P.bq[cap + t] = br.hi;
+        P.bq_idx[t] = (long long)s | ((long long)br.it << 40);
+      } else {  // tail full: finish here
+        cs fo, cf[4];
+        RlmpBounds b;
+        HardStage h;
+        load_unc_entry(P, s, packed, fo, cf, b, h);
+        const cs delta = add(add(cf[0], cf[1]), add(cf[2], cf[3]));
+        if (t < P.hq_cap) P.bq_idx[t] = -1;
+        P.theta[packed & kIdxMask] = bisect_finish(fo, cf, delta, b, h.unc, br, P.gm1, P.audit);
+      }
+    }
+  }
+}
+
+// The bisections k_bisect_unc stopped, finished with exact evaluations.
+__global__ void __launch_bounds__(128, 4) k_bisect_tail(MarchParams P) {
+  const int n = min(P.hq_n[7], P.hq_cap);
+  const long long cap = P.hq_cap;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const long long tp = P.bq_idx[t];
+    if (tp < 0) continue;
+    const int s = (int)(tp & kIdxMask);
     const long long packed = P.cq_idx[s];
-    if (packed < 0) continue;
-    const double* q = P.cq + s;
-    const cs fo = {q[0], q[cap], q[2 * cap], q[3 * cap]};
-    cs cf[4];
-#pragma unroll
-    for (int f = 0; f < 4; ++f)
-      cf[f] = {q[(4 + 4 * f) * cap], q[(5 + 4 * f) * cap], q[(6 + 4 * f) * cap],
-               q[(7 + 4 * f) * cap]};
+    cs fo, cf[4];
     RlmpBounds b;
-    b.rho_lo = q[20 * cap], b.rho_hi = q[21 * cap], b.p_lo = q[22 * cap], b.p_hi = q[23 * cap];
-    b.rho_floor = P.rho_floor_coef;
-    b.p_floor = P.p_floor_coef;
     HardStage h;
-    h.done = false;
-    h.thc = q[24 * cap];
-    h.p0 = q[25 * cap];
-    h.err = q[26 * cap];
-    h.certifiable = h.err >= 0.0;
-    h.er = q[27 * cap];
-    h.mhi = (unsigned)(packed >> 40) & kAllVertices;
-    h.lo_all = ((packed >> 56) & 1) != 0;
-    h.unc = kAllVertices & ~((h.lo_all ? kAllVertices : 0u) & h.mhi);
+    load_unc_entry(P, s, packed, fo, cf, b, h);
     const cs delta = add(add(cf[0], cf[1]), add(cf[2], cf[3]));
-    P.theta[packed & kIdxMask] = bisect_uncertified(fo, cf, delta, b, h, P.gm1, P.audit);
+    P.theta[packed & kIdxMask] = bisect_uncertified(fo, cf, delta, b, h, P.gm1, P.audit, P.bq[t],
+                                                    P.bq[cap + t], (int)(tp >> 40));
   }
 }
 
@@ -806,6 +877,7 @@ cudaError_t launch_theta_hard(const MarchParams& P, cudaStream_t st) {
     k_theta_hard<<<148 * 8, 256, 0, st>>>(P);
     k_bisect_cert<<<148 * 8, 256, 0, st>>>(P);
     k_bisect_unc<<<dim3(148 * 3, 3), 256, 0, st>>>(P);
+    if (P.replay) k_bisect_tail<<<148 * 4, 128, 0, st>>>(P);
   }
   return cudaGetLastError();
 }
