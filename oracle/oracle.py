@@ -147,6 +147,7 @@ class Oracle:
         self.f_mom = f("ensemble_moments", I, [I, I64, DP, DP, DP])
         if self.kind == "vo":
             self.f_theta = f("sim_theta_cell", None, [P, DP])
+            self.f_limcells = f("sim_limiter_cells", I, [P, D, DP])
         if self.kind == "ref":
             self.f_ot = f("ot_oracle", D, [I, DP, DP])
             self.f_fit = f("fit_rate", D, [I, DP, DP])
@@ -317,6 +318,14 @@ class Sim:
         th = np.zeros((self.g.ny, self.g.nx))
         self.o.f_theta(self.h, _dp(th))
         return th
+
+    def limiter_cells(self, a):
+        """Per-cell limiter inputs and theta at speed a (restatement only):
+        (ny*nx, 27) = u_FO, c_w, c_e, c_s, c_n, rho_lo, rho_hi, p_lo, p_hi,
+        rho_floor, p_floor, theta."""
+        out = np.zeros((self.g.ny * self.g.nx, 27))
+        self.o._check(self.o.f_limcells(self.h, a, _dp(out)))
+        return out
 
     def compute_blending(self, a):
         tx = np.zeros((self.g.ny, self.g.nx + 1))

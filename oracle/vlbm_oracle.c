@@ -670,6 +670,36 @@ int vo_sim_compute_blending(vo_sim* s, double a, double* tx, double* ty) {
   return VLBM_OK;
 }
 
+/* The limiter's per-cell inputs at the step with speed a (the pipeline of
+ * compute_blending, solver.hpp:184-191): per interior cell u_FO (4), the face
+ * corrections c_w, c_e, c_s, c_n (16), rho_lo, rho_hi, p_lo, p_hi, rho_floor,
+ * p_floor (rlmp_bounds) and the limiter's theta -- 27 doubles, row-major.
+ * Test hook for the device limiter restatement (tests/cpp/limiter_check). */
+int vo_sim_limiter_cells(vo_sim* s, double a, double* out) {
+  fill_ghosts(s, a);
+  compute_maxwellians(s, a);
+  compute_candidates(s);
+  for (int j = 0; j < s->g.ny; ++j)
+    for (int i = 0; i < s->g.nx; ++i) {
+      double* r = out + 27 * ((size_t)j * s->g.nx + i);
+      const cs fo = CELL(s->ufo, i, j);
+      cs c[4];
+      face_corrections(s, i, j, c);
+      const bounds b = rlmp_bounds(s, i, j);
+      for (int k = 0; k < 4; ++k) r[k] = fo.v[k];
+      for (int f = 0; f < 4; ++f)
+        for (int k = 0; k < 4; ++k) r[4 + 4 * f + k] = c[f].v[k];
+      r[20] = b.rho_lo;
+      r[21] = b.rho_hi;
+      r[22] = b.p_lo;
+      r[23] = b.p_hi;
+      r[24] = b.rho_floor;
+      r[25] = b.p_floor;
+      r[26] = rlmp_theta(s, i, j);
+    }
+  return VLBM_OK;
+}
+
 void vo_sim_theta_cell(vo_sim* s, double* theta) {
   for (int j = 0; j < s->g.ny; ++j)
     for (int i = 0; i < s->g.nx; ++i) theta[(size_t)j * s->g.nx + i] = CELL(s->thc, i, j);

@@ -40,6 +40,7 @@ void vo_sim_get(vo_sim* s, double* u, double* pops);
 int vo_sim_compute_blending(vo_sim* s, double a, double* tx, double* ty);
 int vo_sim_step_with_blending(vo_sim* s, double dt, const double* tx, const double* ty);
 void vo_sim_theta_cell(vo_sim* s, double* theta);
+int vo_sim_limiter_cells(vo_sim* s, double a, double* out);
 
 int vo_run_sample(const vlbm_grid* g, const vlbm_params* p, const vlbm_perturbation* pp, int K,
                   const double* yc, const double* zc, uint64_t seed, double strip,

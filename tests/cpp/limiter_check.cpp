@@ -1,0 +1,104 @@
+// tests/cpp/limiter_check.cpp — TEST INFRASTRUCTURE: the device limiter
+// (paper_2605_25282_b200/csrc/rlmp.cuh, rlmp_replay.cuh) compiled for the host
+// and run on limiter inputs dumped by the C oracle (vo_sim_limiter_cells):
+// every path the kernels take must reproduce the reference's theta bit for bit
+//   plain     rlmp_theta_hard_plain (30 full feasible() steps)
+//   queued    rlmp_hard_stage + bisect_certified / bisect_uncertified (replay off)
+//   replay    rlmp_hard_stage + bisect_replay with at most kReplayInline exact
+//             steps, the rest resumed by bisect_uncertified (k_bisect_tail)
+// and the theta = 1 vertex certificate must never certify an infeasible cell.
+// The audit counters (a re-run of the full feasible() at every step) must
+// stay zero.  Output: one JSON line of counts.
+// usage: limiter_check records.bin   (27 doubles per cell, see vlbm_oracle.h)
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+using std::isfinite;
+#define __device__
+#define __host__
+#define __forceinline__ inline
+static inline int __popc(unsigned x) { return __builtin_popcount(x); }
+static inline int __ffs(int x) { return __builtin_ffs(x); }
+static inline double __longlong_as_double(long long x) {
+  double d;
+  std::memcpy(&d, &x, 8);
+  return d;
+}
+static inline int atomicAdd(int* p, int v) {
+  const int o = *p;
+  *p += v;
+  return o;
+}
+#include "rlmp_replay.cuh"
+
+using namespace vlbm_dev;
+
+static bool same(double a, double b) { return std::memcmp(&a, &b, 8) == 0; }
+
+int main(int argc, char** argv) {
+  if (argc < 3) {
+    std::fprintf(stderr, "usage: limiter_check records.bin gamma\n");
+    return 2;
+  }
+  FILE* f = std::fopen(argv[1], "rb");
+  if (!f) return 2;
+  const double gm1 = std::atof(argv[2]) - 1.0;
+  double r[27];
+  long cells = 0, at_one = 0, cert = 0, cert_bad = 0, hard = 0, bisect = 0, stopped = 0;
+  long bad_plain = 0, bad_queued = 0, bad_replay = 0;
+  int audit[16] = {0};
+  while (std::fread(r, sizeof r, 1, f) == 1) {
+    ++cells;
+    const cs fo = {r[0], r[1], r[2], r[3]};
+    cs cf[4];
+    for (int q = 0; q < 4; ++q) cf[q] = {r[4 + 4 * q], r[5 + 4 * q], r[6 + 4 * q], r[7 + 4 * q]};
+    RlmpBounds b = {r[20], r[21], r[22], r[23], r[24], r[25]};
+    const double want = r[26];
+    const cs delta = add(add(cf[0], cf[1]), add(cf[2], cf[3]));
+    if (diag_ok(1.0, fo, delta, b, gm1)) {
+      const bool ok = vertex_floors_ok(1.0, fo, cf, b, gm1);
+      const bool c = vertices_certified_at_one(fo, pressure(fo, gm1), cf, b.rho_floor, b.p_floor,
+                                               gm1);
+      cert += c;
+      cert_bad += c && !ok;
+      if (ok) {
+        ++at_one;
+        bad_plain += !same(want, 1.0);
+        continue;
+      }
+    }
+    ++hard;
+    bad_plain += !same(rlmp_theta_hard_plain(fo, cf, b, gm1), want);
+    if (!(finite4(fo) && finite4(cf[0]) && finite4(cf[1]) && finite4(cf[2]) && finite4(cf[3]) &&
+          finite4(delta)))
+      continue;  // the kernels take the plain path for these
+    const HardStage h = rlmp_hard_stage(fo, cf, delta, b, gm1);
+    if (h.done) {
+      bad_queued += !same(h.result, want);
+      bad_replay += !same(h.result, want);
+      continue;
+    }
+    ++bisect;
+    const double q = h.unc ? bisect_uncertified(fo, cf, delta, b, h, gm1, audit)
+                           : bisect_certified(fo, delta, b, h.thc, gm1);
+    bad_queued += !same(q, want);
+    Bracket br;
+    double t;
+    if (bisect_replay(fo, cf, delta, b, h, gm1, 2, br, audit)) {
+      t = br.lo;
+    } else {
+      ++stopped;
+      t = bisect_uncertified(fo, cf, delta, b, h, gm1, audit, br.lo, br.hi, br.it);
+    }
+    bad_replay += !same(t, want);
+  }
+  std::fclose(f);
+  std::printf(
+      "{\"cells\": %ld, \"theta_one\": %ld, \"certified_at_one\": %ld, \"certificate_errors\": %ld, "
+      "\"hard\": %ld, \"bisections\": %ld, \"replay_stopped\": %ld, \"mismatch_plain\": %ld, "
+      "\"mismatch_queued\": %ld, \"mismatch_replay\": %ld, \"audit_errors\": %d}\n",
+      cells, at_one, cert, cert_bad, hard, bisect, stopped, bad_plain, bad_queued, bad_replay,
+      audit[0]);
+  return 0;
+}
