@@ -189,8 +189,12 @@ int alloc_batch(const vlbm_grid* g, const vlbm_params* p, int S, int device, vlb
   {
     const size_t n = (size_t)S * vlbm_impl::theta_tiles(P.nx, P.ny) * 8;
     if (n / 8 > (size_t)INT_MAX) rc = set_error(VLBM_E_INVALID, "too many tiles for one batch");
-    chk(cudaMalloc(&P.cert_hint, n), "malloc cert_hint");
-    if (rc == VLBM_OK) chk(cudaMemset(P.cert_hint, 3, n), "memset cert_hint");
+    // VLBM_CERT_HINT=0 (A/B switch): no hints, every warp tries the certificate
+    const char* e = getenv("VLBM_CERT_HINT");
+    if (!e || atoi(e) != 0) {
+      chk(cudaMalloc(&P.cert_hint, n), "malloc cert_hint");
+      if (rc == VLBM_OK) chk(cudaMemset(P.cert_hint, 3, n), "memset cert_hint");
+    }
   }
   int G = S >= 8 ? 2 : 1;
   int sms = 148;
@@ -217,7 +221,8 @@ int alloc_batch(const vlbm_grid* g, const vlbm_params* p, int S, int device, vlb
     Q.theta = P.theta + (size_t)s0 * P.plane;
     Q.inlet = P.inlet + (size_t)s0 * P.ny * 4;
     Q.n_active = b->d_active_g + g;
-    Q.cert_hint = P.cert_hint + (size_t)s0 * vlbm_impl::theta_tiles(P.nx, P.ny) * 8;
+    Q.cert_hint =
+        P.cert_hint ? P.cert_hint + (size_t)s0 * vlbm_impl::theta_tiles(P.nx, P.ny) * 8 : nullptr;
     Q.persist_ctas = std::max(1, sms * vlbm_impl::theta_ctas_per_sm() / G);
     cudaStream_t sg = b->stream;
     if (g > 0) chk(cudaStreamCreateWithFlags(&sg, cudaStreamNonBlocking), "stream g");
