@@ -170,39 +170,43 @@ __device__ __forceinline__ cs staged_m(const double* U, int NU, const double* F,
   return (k & 1) ? sub(wu, a) : add(wu, a);
 }
 
-// Slot of this thread among the flagged threads of the CTA: warp ballot, one
-// shared atomic per warp.  All threads call it.
-__device__ __forceinline__ int block_slot(bool flag, int* counter) {
+// Slot of this lane among the flagged lanes of its warp in a global queue:
+// one atomic on `counter` per warp (by its first flagged lane); returns the
+// warp's base in *wbase and its count in *wcount.  All lanes call it.
+__device__ __forceinline__ int warp_slot(bool flag, int* counter, int* wbase, int* wcount) {
   const unsigned lane = threadIdx.x & 31;
   const unsigned m = __ballot_sync(0xffffffffu, flag);
-  int slot = 0;
+  int base = 0;
   if (m) {
     const int leader = __ffs(m) - 1;
-    int wb = 0;
-    if ((int)lane == leader) wb = atomicAdd(counter, __popc(m));
-    wb = __shfl_sync(0xffffffffu, wb, leader);
-    slot = wb + __popc(m & ((1u << lane) - 1u));
+    if ((int)lane == leader) base = atomicAdd(counter, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, leader);
   }
-  return slot;
+  *wbase = base;
+  *wcount = __popc(m);
+  return base + __popc(m & ((1u << lane) - 1u));
 }
 
-// Append the CTA's hard cells (flag) to the global limiter queue: block-
-// aggregated slots, one global atomic per CTA.  When the queue is full (or
-// absent) the cell finishes in place.  All threads call it.
+// Append the warp's hard cells (flag) to the global limiter queue: warp-
+// aggregated slots, one global atomic per warp with hard cells, no CTA
+// barrier (warps that finish their cells early move on to the next tile).
+// When the queue cannot hold the warp's cells (or is absent) they finish in
+// place.  All lanes of the warp call it.
 __device__ __forceinline__ void enqueue_hard(const MarchParams& P, bool hard, long long cell,
                                              const cs& fo, const cs* cf, const RlmpBounds& b,
-                                             double gm1, int& qn, int& qbase) {
-  __syncthreads();
-  if (threadIdx.x == 0) qn = 0;
-  __syncthreads();
-  const int slot = block_slot(hard, &qn);
-  __syncthreads();
-  if (threadIdx.x == 0) qbase = (qn && P.hq) ? atomicAdd(P.hq_n, qn) : 0;
-  __syncthreads();
+                                             double gm1) {
+  const unsigned lane = threadIdx.x & 31;
+  const unsigned m = __ballot_sync(0xffffffffu, hard);
+  if (!m) return;
+  const int leader = __ffs(m) - 1;
+  int base = 0;
+  if ((int)lane == leader && P.hq) base = atomicAdd(P.hq_n, __popc(m));
+  base = __shfl_sync(0xffffffffu, base, leader);
   if (!hard) return;
-  if (P.hq && qbase + qn <= P.hq_cap) {
+  const int slot = base + __popc(m & ((1u << lane) - 1u));
+  if (P.hq && base + __popc(m) <= P.hq_cap) {
     const long long cap = P.hq_cap;
-    double* q = P.hq + qbase + slot;
+    double* q = P.hq + slot;
     q[0] = fo.r;
     q[cap] = fo.mx;
     q[2 * cap] = fo.my;
@@ -218,9 +222,9 @@ __device__ __forceinline__ void enqueue_hard(const MarchParams& P, bool hard, lo
     q[21 * cap] = b.rho_hi;
     q[22 * cap] = b.p_lo;
     q[23 * cap] = b.p_hi;
-    P.hq_idx[qbase + slot] = cell;
+    P.hq_idx[slot] = cell;
   } else {  // queue full (or absent): finish in place
-    if (P.hq && qbase + slot < P.hq_cap) P.hq_idx[qbase + slot] = -1;
+    if (P.hq && slot < P.hq_cap) P.hq_idx[slot] = -1;
     P.theta[cell] = rlmp_theta_hard(fo, cf, b, gm1, P.audit);  // rare: plain bisection
   }
 }
@@ -239,7 +243,7 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_THETA_MINB)
   using namespace tiled;
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) unsigned long long bar;
-  __shared__ int qn, qbase, s_next;
+  __shared__ int s_next;
   double* R = sm;                    // u [4][NR2] by TMA, then inv2a f/g, p: [9][NR2]
   double* RF = R + kStagedTheta * NR2;  // rfo[NF], pfo[NF]
   double* SP = sm + kThetaSP;        // populations [16][NA] by TMA
@@ -272,10 +276,7 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_THETA_MINB)
   };
   int t = next_active(blockIdx.x);
   if (t >= total) return;
-  if (threadIdx.x == 0) {
-    qn = 0;
-    mbar_init(&bar);
-  }
+  if (threadIdx.x == 0) mbar_init(&bar);
   __syncthreads();
   if (threadIdx.x == 0) issue(t);
   for (unsigned it = 0; t < total; ++it) {
@@ -372,13 +373,12 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_THETA_MINB)
       pfo0 = st.pfo[0];
       delta = add(add(cf[0], cf[1]), add(cf[2], cf[3]));
     }
-    // The staged buffers are free: prefetch the next tile.
+    // The staged buffers are free: prefetch the next tile (claimed before the
+    // barrier, so every thread reads s_next right after it).
+    if (threadIdx.x == 0) s_next = claim(t);
     __syncthreads();
-    if (threadIdx.x == 0) {
-      const int tn = claim(t);
-      s_next = tn;
-      if (tn < total) issue(tn);
-    }
+    const int t_next = s_next;
+    if (threadIdx.x == 0 && t_next < total) issue(t_next);
 
     // feasible(1): the diagonal first; the 15 vertex floors only when the
     // certificate cannot prove them.  Certificate hint of this warp (warp-
@@ -428,8 +428,8 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_THETA_MINB)
       }
     }
     const long long cell = (long long)s * P.plane + (long long)j * P.pitch + i;
-    enqueue_hard(P, hard, cell, foC, cf, b, gm1, qn, qbase);  // starts with __syncthreads
-    t = s_next;
+    enqueue_hard(P, hard, cell, foC, cf, b, gm1);
+    t = t_next;
   }
 }
 
@@ -606,7 +606,6 @@ constexpr int kReplayInline = 2;
 #define VLBM_UNC_MINB 2
 #endif
 __global__ void __launch_bounds__(256, VLBM_UNC_MINB) k_bisect_unc(MarchParams P) {
-  __shared__ int nt, tbase;
   const int third = P.hq_cap / 3;
   const int n = min(P.hq_n[3 + blockIdx.y], third);
   const long long cap = P.hq_cap;
@@ -629,16 +628,11 @@ __global__ void __launch_bounds__(256, VLBM_UNC_MINB) k_bisect_unc(MarchParams P
         P.theta[packed & kIdxMask] = bisect_uncertified(fo, cf, delta, b, h, P.gm1, P.audit);
       }
     }
-    if (!P.replay) continue;  // uniform across the CTA
+    if (!P.replay) continue;
     // stopped bisections -> the tail queue (bq storage; k_bisect_cert is done)
-    if (threadIdx.x == 0) nt = 0;
-    __syncthreads();
-    const int my = stopped ? atomicAdd(&nt, 1) : 0;
-    __syncthreads();
-    if (threadIdx.x == 0) tbase = nt ? atomicAdd(P.hq_n + 7, nt) : 0;
-    __syncthreads();
+    int tbase, nt;
+    const int t = warp_slot(stopped, P.hq_n + 7, &tbase, &nt);
     if (stopped) {
-      const int t = tbase + my;
       if (tbase + nt <= P.hq_cap) {
         P.bq[t] = br.lo;
         P.bq[cap + t] = br.hi;
