@@ -46,7 +46,7 @@ int main(int argc, char** argv) {
   const double gm1 = std::atof(argv[2]) - 1.0;
   double r[27];
   long cells = 0, at_one = 0, cert = 0, cert_bad = 0, hard = 0, bisect = 0, stopped = 0;
-  long bad_plain = 0, bad_queued = 0, bad_replay = 0;
+  long bad_plain = 0, bad_queued = 0, bad_replay = 0, margin_bad = 0;
   int audit[16] = {0};
   while (std::fread(r, sizeof r, 1, f) == 1) {
     ++cells;
@@ -80,6 +80,16 @@ int main(int argc, char** argv) {
       continue;
     }
     ++bisect;
+    {  // every vertex the stage marks as clearing the margins at thc really does
+      const cs t[4] = {scale(h.thc, cf[0]), scale(h.thc, cf[1]), scale(h.thc, cf[2]),
+                       scale(h.thc, cf[3])};
+      for (int S = 1; S < 16; ++S) {
+        if (!(h.mhi >> S & 1)) continue;
+        const cs v = vertex_at(fo, t, S);
+        const double p = pressure(v, gm1);
+        margin_bad += !vertex_margin(p, p, v.r, v.r, b, h.err, h.er);
+      }
+    }
     const double q = h.unc ? bisect_uncertified(fo, cf, delta, b, h, gm1, audit)
                            : bisect_certified(fo, delta, b, h.thc, gm1);
     bad_queued += !same(q, want);
@@ -97,8 +107,9 @@ int main(int argc, char** argv) {
   std::printf(
       "{\"cells\": %ld, \"theta_one\": %ld, \"certified_at_one\": %ld, \"certificate_errors\": %ld, "
       "\"hard\": %ld, \"bisections\": %ld, \"replay_stopped\": %ld, \"mismatch_plain\": %ld, "
-      "\"mismatch_queued\": %ld, \"mismatch_replay\": %ld, \"audit_errors\": %d}\n",
+      "\"mismatch_queued\": %ld, \"mismatch_replay\": %ld, \"audit_errors\": %d, "
+      "\"margin_errors\": %ld}\n",
       cells, at_one, cert, cert_bad, hard, bisect, stopped, bad_plain, bad_queued, bad_replay,
-      audit[0]);
+      audit[0], margin_bad);
   return 0;
 }

@@ -50,5 +50,5 @@ def test_limiter_paths_bit_exact(vo, limiter_check, tmp_path, m, steps, every):
     assert r["replay_stopped"] > 0  # ... including the tail resumption
     assert r["certified_at_one"] > 0
     for k in ("certificate_errors", "mismatch_plain", "mismatch_queued", "mismatch_replay",
-              "audit_errors"):
+              "audit_errors", "margin_errors"):
         assert r[k] == 0, (k, r)
