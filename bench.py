@@ -255,7 +255,7 @@ def main():
     ap.add_argument("--grid", default=None,
                     help="NXxNY instead of configs[1]'s 1000x200 (e.g. 4000x800 = configs[2])")
     ap.add_argument("--no-roofline", action="store_true",
-                    help="skip the one-group per-kernel timing pass")
+                    help="omit the roofline objects")
     ap.add_argument("--ref-seconds", type=float, default=15.0,
                     help="target CPU seconds of the reference-CPU sample")
     args = ap.parse_args()
@@ -307,10 +307,10 @@ def main():
     st1 = sim.stats()
     updates = st1["cell_updates"] - st0["cell_updates"]
     launches = st1["launches"] - st0["launches"]
-    n_theta = args.steps  # one k_theta launch per step (RLMP)
-    theta_ms = st1["ms_theta"] / max(n_theta, 1)
-    adv_ms = st1["ms_advance"] / max(args.steps, 1)
-    sched_ms = st1["ms_sched"] / max(args.steps, 1)
+    # per-kernel device times of the timed region: CUDA events around each
+    # launch on the library stream (one sample group: kernels never overlap)
+    kern = {k: (st1[k] - st0[k]) / args.steps for k in
+            ("ms_theta_tiles", "ms_theta_hard", "ms_advance", "ms_sched")}
     t_max = ms
     upd_total = updates
     if ws > 1:
@@ -322,26 +322,6 @@ def main():
         upd_total = float(uu.item())
     value = upd_total / (t_max * 1e-3)
     sim.close()
-
-    # ---- per-kernel device times for the roofline: the same step window
-    # marched again with one sample group, so no two march kernels overlap
-    # and each launch's CUDA-event time is its own duration.
-    kern = None
-    if not args.no_roofline:
-        os.environ["VLBM_GROUPS"] = "1"
-        r = v.BatchSimulation.jet(g, lat, gas, pp, base_seed=42, m0=rank * M, n_samples=M,
-                                  device=local)
-        del os.environ["VLBM_GROUPS"]
-        if args.t_start > 0:
-            r.run_to(args.t_start)
-        r.step(args.warmup)
-        r.set_timing(True)
-        k0 = r.stats()
-        r.step(args.steps)
-        k1 = r.stats()
-        r.close()
-        kern = {k: (k1[k] - k0[k]) / args.steps for k in
-                ("ms_theta_tiles", "ms_theta_hard", "ms_advance", "ms_sched")}
 
     # ---- e2e through the public API from host buffers ----
     e2e = None
@@ -381,7 +361,7 @@ def main():
         cells_per_launch = M * NX * NY
         step_gbs = BYTES_PER_UPDATE * (updates / (ms * 1e-3)) / 1e9
         roof, fp64 = None, None
-        if kern:
+        if not args.no_roofline:
             # the committed ncu figures were captured on the default workload only
             prof = (fp64_profile() or {}) if (NX, NY, M) == (1000, 200, M_PER_GPU) else {}
             # The collide+stream kernel (BASELINE north_star: "roofline = bytes
@@ -393,8 +373,8 @@ def main():
                     "traffic": prof.get("k_advance_tiled_dram_bytes_per_launch"),
                     "peak_source": src, "bytes_per_cell": BYTES_PER_UPDATE,
                     "cells_per_launch": cells_per_launch, "launch_ms": kern["ms_advance"],
-                    "note": "per-launch times from a one-sample-group pass over the same step "
-                            "window; traffic from profiles/r1_kernels.csv (ncu --set full)"}
+                    "note": "per-launch times: CUDA events around each launch in the timed "
+                            "region; traffic from profiles/r1_kernels.csv (ncu --set full)"}
             # The limiter's tile pass, the longest kernel of the step: FP64-bound.
             t_tiles = kern["ms_theta_tiles"] * 1e-3
             lim_gbs = THETA_BYTES_PER_CELL * cells_per_launch / t_tiles / 1e9
@@ -427,9 +407,8 @@ def main():
             "limiter_roofline": fp64,
             "step_roofline": {"achieved": step_gbs, "peak": hbm, "unit": "GB/s",
                               "frac": step_gbs / hbm, "bytes_per_update": BYTES_PER_UPDATE},
-            "kernel_ms_per_step": {"k_theta": theta_ms, "k_advance": adv_ms, "k_sched": sched_ms,
-                                   "note": "timed region (2 sample groups overlap)"},
-            "kernel_ms_per_step_1group": kern,
+            "kernel_ms_per_step": dict(kern, note="timed region; ms_theta_hard = k_theta_hard + "
+                                                  "k_bisect_cert + k_bisect_unc + k_bisect_tail"),
             "clocks": clk.summary(),
         }
         if e2e:

@@ -23,7 +23,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 TAG = sys.argv[1] if len(sys.argv) > 1 else "r1"
 SRC = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "gpurun_out")
 OUT = os.path.join(ROOT, "profiles")
-KERNELS = ["k_theta_tiled", "k_theta_hard", "k_bisect_cert", "k_bisect_unc", "k_advance_tiled",
+KERNELS = ["k_theta_tiled", "k_theta_hard", "k_bisect_cert", "k_bisect_unc", "k_bisect_tail",
+           "k_advance_tiled",
            "k_sched", "k_w1_tile", "k_ordered_mean", "k_strong_partials"]
 # units of work per launch for the per-item columns: cells of the C2 batch
 # (64 x 1000 x 200) for the march tile kernels, coarse cells (2000 x 400)
@@ -126,7 +127,7 @@ def main():
               "k_advance_tiled_dram_bytes_per_launch": round(1e9 * (adv["dram_read_GB"]
                                                                     + adv["dram_write_GB"])),
               "source": f"profiles/{TAG}_kernels.csv (ncu --set full, C2 64 samples at t=5e-4, "
-                        "one sample group)"}
+                        "default build)"}
         with open(os.path.join(OUT, f"{TAG}_roofline_inputs.json"), "w") as f:
             json.dump(fp, f, indent=1)
     for r in rows:
