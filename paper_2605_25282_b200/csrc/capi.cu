@@ -230,6 +230,7 @@ int alloc_batch(const vlbm_grid* g, const vlbm_params* p, int S, int device, vlb
       size_t cap = (size_t)Q.S * P.nx * P.ny;
       if (cap * entry > avail / 2 / G) cap = avail / 2 / G / entry;
       if (cap > (size_t)INT_MAX / 2) cap = (size_t)INT_MAX / 2;
+      cap = cap / 768 * 768;  // even thirds of whole kHB chunks: 16-B aligned bulk copies
       if (cap >= 1024) {
         Q.hq_cap = (int)cap;
         chk(cudaMalloc(&Q.hq, sizeof(double) * vlbm_dev::kHardWords * cap), "malloc hq");

@@ -93,6 +93,16 @@ __device__ __forceinline__ void tma_load_4d(double* dst, const CUtensorMap* map,
       : "memory");
 }
 
+// 1-D bulk copy global -> shared (16-byte aligned, size a multiple of 16).
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes,
+                                          unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 __device__ __forceinline__ int clampi(int v, int lo, int hi) {
   return v < lo ? lo : (v > hi ? hi : v);
 }
@@ -445,19 +455,21 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_THETA_MINB)
 //   k_bisect_tail   the replayed bisections that need more exact steps
 // Queues use block-aggregated slots (one global atomic per CTA pass); a CTA
 // that would overflow a queue finishes those cells in place.
-__device__ __forceinline__ void load_hard_entry(const MarchParams& P, int slot, cs& fo, cs* cf,
-                                                RlmpBounds& b) {
-  const long long cap = P.hq_cap;
-  const double* q = P.hq + slot;
-  fo = {q[0], q[cap], q[2 * cap], q[3 * cap]};
+// Hard-queue entries staged in shared memory: kHB consecutive slots, one
+// bulk copy per SoA word plane (kHardWords + the cell index).
+constexpr int kHB = 256;
+constexpr size_t kHardSmem = sizeof(double) * kHardWords * kHB + sizeof(long long) * kHB;
+__device__ __forceinline__ void load_hard_staged(const MarchParams& P, const double* H, int t,
+                                                 cs& fo, cs* cf, RlmpBounds& b) {
+  fo = {H[t], H[kHB + t], H[2 * kHB + t], H[3 * kHB + t]};
 #pragma unroll
   for (int f = 0; f < 4; ++f)
-    cf[f] = {q[(4 + 4 * f) * cap], q[(5 + 4 * f) * cap], q[(6 + 4 * f) * cap],
-             q[(7 + 4 * f) * cap]};
-  b.rho_lo = q[20 * cap];
-  b.rho_hi = q[21 * cap];
-  b.p_lo = q[22 * cap];
-  b.p_hi = q[23 * cap];
+    cf[f] = {H[(4 + 4 * f) * kHB + t], H[(5 + 4 * f) * kHB + t], H[(6 + 4 * f) * kHB + t],
+             H[(7 + 4 * f) * kHB + t]};
+  b.rho_lo = H[20 * kHB + t];
+  b.rho_hi = H[21 * kHB + t];
+  b.p_lo = H[22 * kHB + t];
+  b.p_hi = H[23 * kHB + t];
   b.rho_floor = P.rho_floor_coef;
   b.p_floor = P.p_floor_coef;
 }
@@ -471,22 +483,48 @@ __device__ __forceinline__ int unc_class(unsigned unc) {
   return n <= 1 ? 0 : (n == 2 ? 1 : 2);
 }
 
+// Persistent over chunks of kHB queue slots: a chunk's entries arrive in
+// shared memory by bulk copies; once every thread holds its entry in
+// registers the next chunk's copies are issued into the same buffer, so
+// they overlap this chunk's work.
 __global__ void __launch_bounds__(256, 2) k_theta_hard(MarchParams P) {
   __shared__ int nb, nc[3], baseb, basec[3];
+  extern __shared__ __align__(128) double H[];  // [kHardWords][kHB] | idx[kHB]
+  __shared__ __align__(8) unsigned long long bar;
+  long long* HI = reinterpret_cast<long long*>(H + kHardWords * kHB);
   const int n = min(P.hq_n[0], P.hq_cap);
   const long long cap = P.hq_cap;
   const double gm1 = P.gm1;
-  for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
-    const int slot = base + threadIdx.x;
+  const int nchunks = (n + kHB - 1) / kHB;
+  if ((int)blockIdx.x >= nchunks) return;
+  auto issue = [&](int chunk) {  // thread 0
+    const int s0 = chunk * kHB;
+    const unsigned bytes = 8u * (unsigned)((min(kHB, n - s0) + 1) & ~1);  // even count: 16-B
+    mbar_expect_tx(&bar, bytes * (kHardWords + 1));
+    for (int w = 0; w < kHardWords; ++w) bulk_load(H + w * kHB, P.hq + w * cap + s0, bytes, &bar);
+    bulk_load(HI, P.hq_idx + s0, bytes, &bar);
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(&bar);
+    issue(blockIdx.x);
+  }
+  __syncthreads();
+  for (int chunk = blockIdx.x, it = 0; chunk < nchunks; chunk += gridDim.x, ++it) {
+    const int slot = chunk * kHB + threadIdx.x;
     int cls = 0;  // 0: finished here, 1: -> bq, 2: -> cq
     int ccls = 0;  // cq bin
     long long idx = -1;
     cs fo, cf[4], delta;
     RlmpBounds b;
     HardStage h;
-    if (slot < n) idx = P.hq_idx[slot];
+    mbar_wait(&bar, it & 1);
+    if (slot < n) {
+      idx = HI[threadIdx.x];
+      load_hard_staged(P, H, threadIdx.x, fo, cf, b);
+    }
+    __syncthreads();  // the buffer is free: next chunk
+    if (threadIdx.x == 0 && chunk + (int)gridDim.x < nchunks) issue(chunk + gridDim.x);
     if (idx >= 0) {
-      load_hard_entry(P, slot, fo, cf, b);
       delta = add(add(cf[0], cf[1]), add(cf[2], cf[3]));
       if (!(finite4(fo) && finite4(cf[0]) && finite4(cf[1]) && finite4(cf[2]) && finite4(cf[3]) &&
             finite4(delta))) {
@@ -784,6 +822,9 @@ static cudaError_t smem_attrs() {
     cudaError_t e = cudaFuncSetAttribute(k_theta_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)tiled::kThetaSmem);
     if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_theta_hard, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)kHardSmem);
+    if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k_advance_tiled<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)tiled::kAdvanceSmem);
     if (e == cudaSuccess)
@@ -867,8 +908,9 @@ int theta_ctas_per_sm() {
 }
 
 cudaError_t launch_theta_hard(const MarchParams& P, cudaStream_t st) {
+  if (cudaError_t e = smem_attrs()) return e;
   if (P.hq) {
-    k_theta_hard<<<148 * 8, 256, 0, st>>>(P);
+    k_theta_hard<<<148 * 2, 256, kHardSmem, st>>>(P);
     k_bisect_cert<<<148 * 8, 256, 0, st>>>(P);
     k_bisect_unc<<<dim3(148 * 3, 3), 256, 0, st>>>(P);
     if (P.replay) k_bisect_tail<<<148 * 4, 128, 0, st>>>(P);
