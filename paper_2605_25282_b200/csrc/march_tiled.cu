@@ -268,12 +268,16 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_THETA_MINB)
   // thread 0: the next tile of this CTA -- claimed from the step's tile
   // counter (hq_n[6], reset by k_sched) so CTAs stay balanced whatever the
   // per-tile cost (boundary tiles, hard cells); static striding without queues
-  auto claim = [&](int t) {
-    if (!P.hq_n) return next_active(t + (int)gridDim.x);
-    int tn;
-    do {
-      tn = (int)gridDim.x + atomicAdd(P.hq_n + 6, 1);
-    } while (tn < total && !P.ctl[tn / per_sample].active);
+  // The claim's atomic is issued at the top of the tile (claim_start) and its
+  // result used only before the prefetch barrier (claim_finish), so its
+  // round trip overlaps the tile's work.
+  auto claim_start = [&](int t) {
+    return P.hq_n ? (int)gridDim.x + atomicAdd(P.hq_n + 6, 1) : next_active(t + (int)gridDim.x);
+  };
+  auto claim_finish = [&](int tn) {
+    if (P.hq_n)
+      while (tn < total && !P.ctl[tn / per_sample].active)
+        tn = (int)gridDim.x + atomicAdd(P.hq_n + 6, 1);
     return tn;
   };
   auto issue = [&](int t) {  // thread 0: the tile's TMA loads
@@ -297,6 +301,8 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_THETA_MINB)
     const double* src = state_src(P, s, parity);
     const double* rows = P.inlet + (long long)s * P.ny * 4;
     const double inv2a = 0.5 / c->a;
+    int tn_claim = 0;
+    if (threadIdx.x == 0) tn_claim = claim_start(t);
     mbar_wait(&bar, it & 1u);
     if (!(x0 >= 2 && x0 + TX + 2 <= P.nx && y0 >= 2 && y0 + TY + 2 <= P.ny)) {
       patch_box<false>(P, src, rows, R, RX2, RY2, x0 - 2, y0 - 2, inv2a);
@@ -385,7 +391,7 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_THETA_MINB)
     }
     // The staged buffers are free: prefetch the next tile (claimed before the
     // barrier, so every thread reads s_next right after it).
-    if (threadIdx.x == 0) s_next = claim(t);
+    if (threadIdx.x == 0) s_next = claim_finish(tn_claim);
     __syncthreads();
     const int t_next = s_next;
     if (threadIdx.x == 0 && t_next < total) issue(t_next);
