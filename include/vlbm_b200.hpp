@@ -12,6 +12,7 @@
 //   run_ensemble(cfg, ...)      ->  vlbm::gpu::run_ensemble(cfg, ...)    ensemble.hpp:235
 //   wasserstein1 / strong_error / restrict_field / ensemble_moments /
 //   compute_metrics             ->  vlbm::gpu::<same name>              metrics.hpp:29-327
+//   cmd_render (CLI render)     ->  vlbm::gpu::render                   vlbm_main.cpp:67-108
 // Same arguments, results (bit-identical), exceptions and files: the
 // manifest and the .vlbm snapshots are written by the reference's own
 // write_manifest / write_snapshot.
@@ -25,6 +26,9 @@
 #include <vector>
 
 #include "vlbm_b200.h"
+// the reference headers this drop-in builds on (render.hpp pulls in
+// metrics.hpp, ensemble.hpp and solver.hpp)
+#include "vlbm/render.hpp"
 
 namespace vlbm::gpu {
 
@@ -365,6 +369,44 @@ inline MetricsReport compute_metrics(const EnsembleManifest& man) {
     rep.rates.push_back(rr);
   }
   return rep;
+}
+
+// The CLI's render command (tools/vlbm_main.cpp cmd_render) with the
+// ensemble moments on the device: what = "sample:M", "mean" or "std"; the
+// PPM is written by the reference's render_ppm (render.hpp:52-80).  Same
+// arguments, exceptions and output file.
+inline void render(const EnsembleManifest& man, int time_index, const std::string& what,
+                   std::string grid_label, const std::string& variable, const std::string& out) {
+  const CaseConfig& cfg = man.config;
+  if (grid_label.empty()) grid_label = cfg.make_grid(cfg.grids.size() - 1).label();
+  const std::size_t gi = man.grid_index(grid_label);
+  if (time_index < 0 || time_index >= static_cast<int>(cfg.snapshot_times.size()))
+    throw std::runtime_error("render: time index out of range");
+  const Variable var = variable_from_name(variable);
+  FieldSnapshot field;
+  if (what.rfind("sample:", 0) == 0) {
+    const int m = std::stoi(what.substr(7));
+    if (m < 0 || m >= static_cast<int>(man.samples.size()))
+      throw std::runtime_error("render: sample index out of range");
+    if (man.samples[m].status[gi] != RunStatus::Admissible)
+      throw std::runtime_error("render: sample " + std::to_string(m) + " on grid " + grid_label +
+                               " is not admissible");
+    field = read_snapshot(man.root / man.samples[m].files[gi][time_index], cfg.make_grid(gi));
+  } else if (what == "mean" || what == "std") {
+    std::vector<FieldSnapshot> fields;
+    for (const SampleRecord& r : man.samples) {
+      if (r.status[gi] != RunStatus::Admissible) continue;
+      fields.push_back(read_snapshot(man.root / r.files[gi][time_index], cfg.make_grid(gi)));
+    }
+    if (fields.size() < 2) throw std::runtime_error("render: need >= 2 admissible samples");
+    std::vector<const FieldSnapshot*> ptrs;
+    for (const auto& f : fields) ptrs.push_back(&f);
+    auto [mean, stddev] = gpu::ensemble_moments(ptrs);
+    field = what == "mean" ? std::move(mean) : std::move(stddev);
+  } else {
+    throw std::runtime_error("render: --what must be sample:M, mean, or std");
+  }
+  render_ppm(field, var, cfg.render_floor, cfg.colormap, out);
 }
 
 }  // namespace vlbm::gpu

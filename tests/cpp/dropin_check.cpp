@@ -10,6 +10,9 @@
 //                                   output directories (manifest + snapshots)
 //   dropin_check metrics <dir>      compute_metrics vs gpu::compute_metrics on
 //                                   that ensemble: identical rows (bitwise)
+//   dropin_check outputs <dir>      metrics / rates CSVs (write_metrics_csv) and
+//                                   rendered PPMs (cmd_render vs gpu::render:
+//                                   mean, std, sample; rho, energy) byte-identical
 #include <cstdio>
 #include <cstring>
 #include <filesystem>
@@ -18,6 +21,7 @@
 #include <sstream>
 
 #include "vlbm/metrics.hpp"
+#include "vlbm/render.hpp"
 #include "vlbm_b200.hpp"
 
 using namespace vlbm;
@@ -124,6 +128,62 @@ static int check_metrics(const fs::path& dir) {
   return bad ? 1 : 0;
 }
 
+static std::string file_bytes(const fs::path& p) {
+  std::ifstream f(p, std::ios::binary);
+  return std::string(std::istreambuf_iterator<char>(f), {});
+}
+
+// The metrics / rates CSVs (write_metrics_csv over the two reports) and the
+// rendered PPMs (cmd_render's path vs gpu::render) must be byte-identical.
+static int check_outputs(const fs::path& dir) {
+  const EnsembleManifest man = read_manifest(dir / "run" / "manifest.txt");
+  const MetricsReport want = compute_metrics(man);
+  const MetricsReport got = gpu::compute_metrics(man);
+  write_metrics_csv(want, dir / "cpu_metrics.csv", dir / "cpu_rates.csv");
+  write_metrics_csv(got, dir / "gpu_metrics.csv", dir / "gpu_rates.csv");
+  int bad = 0;
+  for (const char* k : {"metrics", "rates"}) {
+    const bool same = file_bytes(dir / (std::string("cpu_") + k + ".csv")) ==
+                      file_bytes(dir / (std::string("gpu_") + k + ".csv"));
+    bad += !same;
+    std::printf("%s csv: %s\n", k, same ? "identical" : "DIFFERS");
+  }
+  const CaseConfig& cfg = man.config;
+  int renders = 0;
+  for (std::size_t gi = 0; gi < cfg.grids.size(); ++gi) {
+    const std::string label = cfg.make_grid(gi).label();
+    for (int ti = 0; ti < static_cast<int>(cfg.snapshot_times.size()); ++ti) {
+      for (const std::string what : {"mean", "std", "sample:3"}) {
+        for (const std::string var : {"rho", "energy"}) {
+          // the reference's cmd_render path: host ensemble_moments + render_ppm
+          FieldSnapshot field;
+          if (what == "sample:3") {
+            field = read_snapshot(man.root / man.samples[3].files[gi][ti], cfg.make_grid(gi));
+          } else {
+            std::vector<FieldSnapshot> fields;
+            for (const SampleRecord& r : man.samples)
+              if (r.status[gi] == RunStatus::Admissible)
+                fields.push_back(read_snapshot(man.root / r.files[gi][ti], cfg.make_grid(gi)));
+            std::vector<const FieldSnapshot*> ptrs;
+            for (const auto& f : fields) ptrs.push_back(&f);
+            auto [mean, stddev] = ensemble_moments(ptrs);
+            field = what == "mean" ? mean : stddev;
+          }
+          const fs::path a = dir / "cpu.ppm", b = dir / "gpu.ppm";
+          render_ppm(field, variable_from_name(var), cfg.render_floor, cfg.colormap, a.string());
+          gpu::render(man, ti, what, label, var, b.string());
+          const bool same = file_bytes(a) == file_bytes(b);
+          bad += !same;
+          ++renders;
+          if (!same) std::printf("render %s t%d %s %s DIFFERS\n", label.c_str(), ti, what.c_str(), var.c_str());
+        }
+      }
+    }
+  }
+  std::printf("renders: %d compared, %d differ\n", renders, bad);
+  return bad ? 1 : 0;
+}
+
 int main(int argc, char** argv) {
   if (argc < 2) return 2;
   const std::string mode = argv[1];
@@ -132,6 +192,7 @@ int main(int argc, char** argv) {
     if (mode == "nogpu") return check_nogpu();
     if (mode == "ensemble" && argc >= 3) return check_ensemble(argv[2], argc > 3 ? std::atoi(argv[3]) : 8);
     if (mode == "metrics" && argc >= 3) return check_metrics(argv[2]);
+    if (mode == "outputs" && argc >= 3) return check_outputs(argv[2]);
   } catch (const std::exception& e) {
     std::printf("exception: %s\n", e.what());
     return 3;

@@ -50,7 +50,9 @@ def test_gpu_run_ensemble_byte_identical_to_reference_and_metrics():
     """SURVEY §7.2 step 2 gate: the GPU run_ensemble writes a byte-identical
     output directory (manifest + every .vlbm snapshot) to the reference's CPU
     run_ensemble on a smoke-style case (125x25 and 250x50, M=8, t = 0..0.003);
-    then compute_metrics on device equals the reference's bit-for-bit."""
+    then compute_metrics on device equals the reference's bit-for-bit, and
+    the metrics / rates CSVs and the CLI render output (mean / std / sample
+    PPMs through gpu::render) are byte-identical."""
     if not os.path.exists(BIN):
         pytest.skip("dropin_check not built")
     d = tempfile.mkdtemp(prefix="vlbm_dropin_")
@@ -59,5 +61,7 @@ def test_gpu_run_ensemble_byte_identical_to_reference_and_metrics():
         assert rc == 0, out
         rc, out = _run("metrics", d)
         assert rc == 0, out
+        rc, out = _run("outputs", d)  # CSVs + rendered PPMs byte-identical
+        assert rc == 0 and "renders:" in out, out
     finally:
         shutil.rmtree(d, ignore_errors=True)
