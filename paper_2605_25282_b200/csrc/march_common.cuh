@@ -129,12 +129,23 @@ __device__ __forceinline__ void reduce_signal(SampleCtl* c, unsigned long long b
 }
 
 
+#ifndef VLBM_STORE_CS
+#define VLBM_STORE_CS 1
+#endif
 __device__ __forceinline__ void store_plane4(double* base, long long plane, long long off,
                                              const cs& v) {
+#if VLBM_STORE_CS  // streaming (evict-first) stores: the new state is not re-read
+                   // before it leaves L2, the old state's lines stay for the pulls
+  __stcs(base + off, v.r);
+  __stcs(base + plane + off, v.mx);
+  __stcs(base + 2 * plane + off, v.my);
+  __stcs(base + 3 * plane + off, v.e);
+#else
   base[off] = v.r;
   base[plane + off] = v.mx;
   base[2 * plane + off] = v.my;
   base[3 * plane + off] = v.e;
+#endif
 }
 
 // ---------------------------------------------------------------------------
