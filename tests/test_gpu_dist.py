@@ -66,3 +66,26 @@ def test_nccl_reshard_w1_l1_bit_exact(vo, nccl_group, M, ny, nx):
     B[:, 0] = fine_r[valid].reshape(-1, ny, nx)
     assert float(w1).hex() == vo.wasserstein1(A, B, 0).hex()
     assert float(es).hex() == vo.strong_error(A, B)[0].hex()
+
+
+def test_bench_sharded_postproc_matches_single_device(nccl_group):
+    """bench.py's sharded configs[3] leg (restriction, NCCL re-shard by cell,
+    per-cell terms, ordered gather, sequential mean) gives the single-device
+    W1 of the same synthetic ensembles, bit for bit."""
+    import importlib.util
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(root, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    M, nxc, nyc = 64, 50, 20
+    r = bench.postproc_bench_dist(torch, dist, 0, 1, 0, M=M, nxc=nxc, nyc=nyc, reps=1)
+    dev = "cuda:0"
+    gen = torch.Generator(device=dev)
+    coarse = torch.empty((M, nyc, nxc), dtype=torch.float64, device=dev)
+    fine = torch.empty((M, 2 * nyc, 2 * nxc), dtype=torch.float64, device=dev)
+    gen.manual_seed(1000)
+    coarse.normal_(-0.125, 0.5, generator=gen).exp_()
+    gen.manual_seed(1001)
+    fine.normal_(-0.125, 0.5, generator=gen).exp_()
+    assert float(r["W1"]).hex() == float(post.wasserstein1(torch, coarse, fine)).hex()
+    assert r["w1_cells_per_s"] > 0
