@@ -730,7 +730,6 @@ int vlbm_wasserstein1(int M, int64_t n, const double* a, const double* b, int va
   if (M < 1 || !a || !b || !result)
     return set_error(VLBM_E_INVALID, "wasserstein1: sample counts differ or are empty");
   if (var < 0 || var > 3) return set_error(VLBM_E_INVALID, "variable must be 0..3");
-  if (M > 1024) return set_error(VLBM_E_INVALID, "wasserstein1: M > 1024 not supported");
   if (int rc = current_device()) return rc;
   DevBuf da, db, dt, dr;
   if (int rc = upload(da, a, (size_t)4 * n * M)) return rc;
@@ -785,7 +784,7 @@ int vlbm_strong_finish(int M, const double* partials, double* result, double* pe
 
 int vlbm_d_w1_restrict(int M, int nxc, int nyc, const double* d_coarse, int64_t c_stride,
                        const double* d_fine, int64_t f_stride, double* d_terms, void* stream) {
-  if (M < 1 || M > 1024) return set_error(VLBM_E_INVALID, "wasserstein1: 1 <= M <= 1024");
+  if (M < 1) return set_error(VLBM_E_INVALID, "wasserstein1: sample counts differ or are empty");
   CU(vlbm_impl::launch_w1_restrict(M, nxc, nyc, d_coarse, c_stride, d_fine, f_stride, d_terms,
                                    (cudaStream_t)stream));
   return VLBM_OK;
@@ -799,14 +798,14 @@ int vlbm_d_restrict_var(int M, int nxc, int nyc, const double* d_fine, int var, 
 
 int vlbm_d_w1_cells(int M, int64_t n, const double* d_a, const double* d_b, double* d_terms,
                     void* stream) {
-  if (M < 1 || M > 1024) return set_error(VLBM_E_INVALID, "wasserstein1: 1 <= M <= 1024");
+  if (M < 1) return set_error(VLBM_E_INVALID, "wasserstein1: sample counts differ or are empty");
   CU(vlbm_impl::launch_w1_cells(M, n, d_a, d_b, d_terms, (cudaStream_t)stream));
   return VLBM_OK;
 }
 
 int vlbm_d_w1_cells_planes(int M, int64_t n, const double* d_a, const double* d_b,
                            double* d_terms, void* stream) {
-  if (M < 1 || M > 1024) return set_error(VLBM_E_INVALID, "wasserstein1: 1 <= M <= 1024");
+  if (M < 1) return set_error(VLBM_E_INVALID, "wasserstein1: sample counts differ or are empty");
   CU(vlbm_impl::launch_w1_planes(M, n, d_a, n, d_b, n, d_terms, (cudaStream_t)stream));
   return VLBM_OK;
 }

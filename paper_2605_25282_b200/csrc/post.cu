@@ -6,9 +6,10 @@
 //                                 the reference's sequential order; the
 //                                 restriction of the fine sample is fused
 //   k_w1_*                        wasserstein1's per-cell term (:113-122):
-//                                 warp-per-cell bitonic sort of M <= 1024
+//                                 warp-per-cell sort of M <= 1024
 //                                 order-preserving 64-bit keys in registers,
-//                                 then the sequential sum over ranks
+//                                 then the sequential sum over ranks; M > 1024:
+//                                 cell-major keys + CUB segmented sort
 //   k_ordered_mean                wasserstein1's storage-order acc (:122-124)
 //   k_moments                     ensemble_moments (:148-177)
 //
@@ -18,7 +19,11 @@
 // so only the add latency is on the critical path.
 #include <cuda_runtime.h>
 
+#include <cub/device/device_segmented_sort.cuh>
+
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -538,11 +543,127 @@ cudaError_t launch_strong_partials_var(int M, int nxc, int nyc, const double* co
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// W1 for M > 1024 (any ensemble size): cells in batches; both ensembles of a
+// batch transposed to cell-major order-preserving keys (32x32 tiles through
+// shared memory: coalesced reads along cells, writes along samples; the
+// restriction of the fine ensemble fused as in k_w1_tile), each cell's M keys
+// sorted by CUB's segmented sort, then one thread per cell adds
+// |a_(m) - b_(m)| strictly in rank order (metrics.hpp:118-122).
+template <int kKind>
+__global__ void k_w1_keys(int M, long long c0, long long nb, int nxc, const double* a,
+                          long long as, const double* b, long long bs, unsigned long long* ka,
+                          unsigned long long* kb) {
+  __shared__ unsigned long long ta[32][33], tb[32][33];
+  const long long cb = (long long)blockIdx.x * 32;  // batch-local cell tile
+  const int mb = blockIdx.y * 32;                    // sample tile
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads
+  for (int r = ty; r < 32; r += 8) {  // read: sample mb + r, cell cb + tx
+    const int m = mb + r;
+    const long long cl = cb + tx, c = c0 + cl;
+    unsigned long long va = 0, vb = 0;
+    if (m < M && cl < nb) {
+      if (kKind == 2) {
+        va = dkey(a[c * M + m]);
+        vb = dkey(b[c * M + m]);
+      } else {
+        va = dkey(a[(long long)m * as + c]);
+        if (kKind == 1) {
+          const int j = (int)(c / nxc), i = (int)(c - (long long)j * nxc);
+          vb = dkey(restrict_at(b + (long long)m * bs, 2 * nxc, i, j));
+        } else {
+          vb = dkey(b[(long long)m * bs + c]);
+        }
+      }
+    }
+    ta[r][tx] = va;
+    tb[r][tx] = vb;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {  // write: cell cb + r, sample mb + tx
+    const long long cl = cb + r;
+    const int m = mb + tx;
+    if (m < M && cl < nb) {
+      ka[cl * M + m] = ta[tx][r];
+      kb[cl * M + m] = tb[tx][r];
+    }
+  }
+}
+
+__global__ void k_w1_sorted_terms(int M, long long nb, const unsigned long long* ka,
+                                  const unsigned long long* kb, double* terms) {
+  for (long long cl = (long long)blockIdx.x * blockDim.x + threadIdx.x; cl < nb;
+       cl += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long* pa = ka + cl * M;
+    const unsigned long long* pb = kb + cl * M;
+    double cell = 0.0;
+    for (int m = 0; m < M; ++m) cell += fabs(dval(pa[m]) - dval(pb[m]));
+    terms[cl] = cell / static_cast<double>(M);
+  }
+}
+
+__global__ void k_seg_offsets(int M, long long nb, int* off) {  // segment c starts at c * M
+  for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c <= nb;
+       c += (long long)gridDim.x * blockDim.x)
+    off[c] = (int)(c * M);
+}
+
+template <int kKind>
+static cudaError_t launch_w1_large(int M, long long n, int nxc, const double* a, long long as,
+                                   const double* b, long long bs, double* terms,
+                                   cudaStream_t st) {
+  // batch: 4 key arrays (two ensembles, sorted copies) of M x nb keys within
+  // ~4 GB and under CUB's 32-bit item count
+  long long nb_max = (4ll << 30) / (32ll * M);
+  nb_max = nb_max < (0x7fffffffll / M) ? nb_max : (0x7fffffffll / M);
+  nb_max = nb_max < n ? nb_max : n;
+  if (const char* e = getenv("VLBM_W1_BATCH_CELLS"))  // test hook: force several batches
+    nb_max = std::max(1ll, std::min(nb_max, atoll(e)));
+  if (nb_max < 1) return cudaErrorInvalidValue;
+  const size_t items = (size_t)M * nb_max;
+  unsigned long long *ka = nullptr, *kb = nullptr, *sa = nullptr, *sb = nullptr;
+  void* tmp = nullptr;
+  int* off = nullptr;
+  size_t tmp_bytes = 0;
+  cudaError_t e = cub::DeviceSegmentedSort::SortKeys(nullptr, tmp_bytes, ka, sa, (int)items,
+                                                     (int)nb_max, off, off + 1, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&off, sizeof(int) * (nb_max + 1), st);
+  if (e == cudaSuccess) {
+    k_seg_offsets<<<(unsigned)((nb_max + 256) / 256), 256, 0, st>>>(M, nb_max, off);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMallocAsync(&ka, items * 8, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&kb, items * 8, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&sa, items * 8, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&sb, items * 8, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&tmp, tmp_bytes, st);
+  for (long long c0 = 0; e == cudaSuccess && c0 < n; c0 += nb_max) {
+    const long long nb = (n - c0) < nb_max ? (n - c0) : nb_max;
+    const int nitems = (int)(M * nb);
+    const dim3 g((unsigned)((nb + 31) / 32), (unsigned)((M + 31) / 32));
+    k_w1_keys<kKind><<<g, 256, 0, st>>>(M, c0, nb, nxc, a, as, b, bs, ka, kb);
+    e = cudaGetLastError();
+    size_t tb = tmp_bytes;
+    if (e == cudaSuccess)
+      e = cub::DeviceSegmentedSort::SortKeys(tmp, tb, ka, sa, nitems, (int)nb, off, off + 1, st);
+    if (e == cudaSuccess)
+      e = cub::DeviceSegmentedSort::SortKeys(tmp, tb, kb, sb, nitems, (int)nb, off, off + 1, st);
+    if (e == cudaSuccess) {
+      k_w1_sorted_terms<<<(unsigned)((nb + 255) / 256), 256, 0, st>>>(M, nb, sa, sb, terms + c0);
+      e = cudaGetLastError();
+    }
+  }
+  for (void* p : {(void*)ka, (void*)kb, (void*)sa, (void*)sb, tmp, (void*)off})
+    if (p) cudaFreeAsync(p, st);
+  return e;
+}
+
 // W1 launch for M <= 1024: R = keys per lane (next power of two of M/32).
 template <int kKind>
 static cudaError_t launch_w1(int M, long long n, int nxc, const double* a, long long as,
                              const double* b, long long bs, double* terms, cudaStream_t st) {
-  if (M < 1 || M > 1024) return cudaErrorInvalidValue;
+  if (M < 1) return cudaErrorInvalidValue;
+  if (M > 1024) return launch_w1_large<kKind>(M, n, nxc, a, as, b, bs, terms, st);
   const int grid = (int)((n + kW1Cells - 1) / kW1Cells);
   auto go = [&](auto kernel, int R, int nbuf) {
     const size_t smem = sizeof(double) * nbuf * kW1Cells * (32 * R + 32);

@@ -36,7 +36,7 @@ def nccl_group():
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("M,ny,nx", [(11, 3, 7), (64, 20, 50), (1000, 4, 8)])
+@pytest.mark.parametrize("M,ny,nx", [(11, 3, 7), (64, 20, 50), (1000, 4, 8), (1300, 4, 8)])
 def test_nccl_reshard_w1_l1_bit_exact(vo, nccl_group, M, ny, nx):
     rng = np.random.default_rng(M)
     coarse = rng.lognormal(-0.125, 0.5, size=(M, ny, nx))

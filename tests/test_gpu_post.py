@@ -69,7 +69,7 @@ def test_strong_error_kats(vlbm):
         vlbm.strong_error(a, np.zeros((0, 4, 4, 4)))
 
 
-@pytest.mark.parametrize("M", [1, 2, 5, 31, 32, 33, 64, 100, 257, 1000])
+@pytest.mark.parametrize("M", [1, 2, 5, 31, 32, 33, 64, 100, 257, 1000, 1025, 2500])
 @pytest.mark.parametrize("ties", [False, True])
 def test_wasserstein1_bitwise(vlbm, oc, M, ties):
     rng = np.random.default_rng(M + 7 * ties)
@@ -142,8 +142,8 @@ def test_moments_bitwise(vlbm, oc, M):
         vlbm.ensemble_moments(x[:1])
 
 
-@pytest.mark.parametrize("M,nxc,nyc", [(5, 6, 4), (64, 20, 6), (1000, 8, 4)])
-def test_device_pipeline_c4_style(vlbm, oc, M, nxc, nyc):
+@pytest.mark.parametrize("M,nxc,nyc", [(5, 6, 4), (64, 20, 6), (1000, 8, 4), (1500, 10, 6)])
+def test_device_pipeline_c4_style(vlbm, oc, M, nxc, nyc, monkeypatch):
     """Density-plane pipeline (fused restriction) == reference
     wasserstein1(coarse, restrict_field(fine)) and strong_error with the
     other components zero, bit-for-bit."""
@@ -154,6 +154,8 @@ def test_device_pipeline_c4_style(vlbm, oc, M, nxc, nyc):
     f = rng.lognormal(-0.125, 0.5, size=(M, 2 * nyc, 2 * nxc))
     tc = torch.from_numpy(c).cuda()
     tf = torch.from_numpy(f).cuda()
+    if M > 1024:  # the segmented-sort path in several cell batches
+        monkeypatch.setenv("VLBM_W1_BATCH_CELLS", "17")
     w1 = post.wasserstein1(torch, tc, tf)
     es = post.strong_error(torch, tc, tf)
     C4 = np.zeros((M, 4, nyc, nxc))
