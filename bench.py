@@ -264,10 +264,33 @@ def postproc_bench_dist(torch, dist, dev, ws, rank, M=1000, nxc=2000, nyc=400, r
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         times.append(float(t.item()))
     ms = statistics.median(times)
+
+    def timed(fn):
+        fn()
+        ts = []
+        for _ in range(reps):
+            dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            r = fn()
+            e1.record()
+            torch.cuda.synchronize()
+            t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=d)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ts.append(float(t.item()))
+        return r, statistics.median(ts)
+
+    # the fused alternative: no re-shard, each rank's kernel reads the other
+    # ranks' planes through CUDA-IPC peer mappings (NVLink) while it sorts
+    w1p, msp = timed(lambda: vd.peer_wasserstein1(torch, dist, coarse, fine, valid, nxc))
     return {"workload": f"C4 synthetic log-normal rho, M={M} sharded over {ws} ranks, coarse "
                         f"{nxc}x{nyc} vs restricted fine {2 * nxc}x{2 * nyc}; restriction + "
                         "2 NCCL all_to_all + per-cell terms + ordered gather + sequential mean",
-            "w1_cells_per_s": nc / (ms * 1e-3), "w1_ms": ms, "W1": w1, "n_gpus": ws}
+            "w1_cells_per_s": nc / (ms * 1e-3), "w1_ms": ms, "W1": w1, "n_gpus": ws,
+            "peer": {"how": "vlbm_d_w1_rows over CUDA-IPC peer mappings (no all_to_all)",
+                     "w1_cells_per_s": nc / (msp * 1e-3), "w1_ms": msp, "W1": w1p,
+                     "identical": (w1p == w1) if rank == 0 else None}}
 
 
 def run_reference_arm(args):

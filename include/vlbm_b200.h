@@ -263,6 +263,22 @@ int vlbm_d_w1_cells(int M, int64_t n_cells, const double* d_a, const double* d_b
  * gathers the per-cell columns itself. */
 int vlbm_d_w1_cells_planes(int M, int64_t n_cells, const double* d_a, const double* d_b,
                            double* d_cell_terms, void* stream);
+/* Per-cell W1 terms of cells [cell0, cell0 + n_cells) of an nxc-wide coarse
+ * grid over M samples given as ROW TABLES: d_coarse_rows / d_fine_rows are
+ * device arrays of M device pointers, sample m's coarse density plane and
+ * its fine (2nxc-wide) plane, which may live on any GPU of the node
+ * (peer-mapped through vlbm_ipc_open).  The restriction is fused; the kernel
+ * reads the remote samples over NVLink while it sorts (the fused alternative
+ * to the all-to-all re-shard; wasserstein1's per-cell term, metrics.hpp:113-122). */
+int vlbm_d_w1_rows(int M, int nxc, int64_t cell0, int64_t n_cells,
+                   const double* const* d_coarse_rows, const double* const* d_fine_rows,
+                   double* d_cell_terms, void* stream);
+/* CUDA IPC for the row tables: the 64-byte handle of the allocation holding
+ * d_ptr and d_ptr's byte offset in it; open a peer process's handle (the
+ * base of its allocation, mapped with peer access) and close it. */
+int vlbm_ipc_handle(const void* d_ptr, unsigned char handle[64], uint64_t* offset);
+int vlbm_ipc_open(const unsigned char handle[64], void** d_base);
+int vlbm_ipc_close(void* d_base);
 /* Storage-order sequential sum of n terms, then / n (wasserstein1's acc). */
 int vlbm_d_ordered_mean(int64_t n, const double* d_terms, double* d_result, void* stream);
 /* Per-cell moments on sample-major planes (M x n_cells, one variable). */

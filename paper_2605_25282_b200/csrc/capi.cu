@@ -5,6 +5,7 @@
 // There is no CPU fallback: every numeric result below is produced by the
 // sm_100a kernels in march.cu / post.cu; a CUDA failure is reported as
 // VLBM_E_CUDA.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -807,6 +808,55 @@ int vlbm_d_w1_cells_planes(int M, int64_t n, const double* d_a, const double* d_
                            double* d_terms, void* stream) {
   if (M < 1) return set_error(VLBM_E_INVALID, "wasserstein1: sample counts differ or are empty");
   CU(vlbm_impl::launch_w1_planes(M, n, d_a, n, d_b, n, d_terms, (cudaStream_t)stream));
+  return VLBM_OK;
+}
+
+int vlbm_d_w1_rows(int M, int nxc, int64_t cell0, int64_t n, const double* const* d_coarse_rows,
+                   const double* const* d_fine_rows, double* d_terms, void* stream) {
+  if (M < 1) return set_error(VLBM_E_INVALID, "wasserstein1: sample counts differ or are empty");
+  if (nxc < 1 || cell0 < 0 || n < 0 || !d_coarse_rows || !d_fine_rows)
+    return set_error(VLBM_E_INVALID, "wasserstein1: invalid row tables");
+  if (n == 0) return VLBM_OK;
+  CU(vlbm_impl::launch_w1_rows(M, nxc, cell0, n, d_coarse_rows, d_fine_rows, d_terms,
+                               (cudaStream_t)stream));
+  return VLBM_OK;
+}
+
+int vlbm_ipc_handle(const void* d_ptr, unsigned char handle[64], uint64_t* offset) {
+  if (!d_ptr || !handle || !offset) return set_error(VLBM_E_INVALID, "ipc: null argument");
+  using Range = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static Range range = nullptr;
+  if (!range) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        !fn)
+      return set_error(VLBM_E_CUDA, "ipc: cuMemGetAddressRange unavailable");
+    range = reinterpret_cast<Range>(fn);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, (CUdeviceptr)d_ptr) != CUDA_SUCCESS)
+    return set_error(VLBM_E_CUDA, "ipc: not a device allocation");
+  cudaIpcMemHandle_t h;
+  CU(cudaIpcGetMemHandle(&h, (void*)base));
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  std::memcpy(handle, &h, 64);
+  *offset = (uint64_t)((CUdeviceptr)d_ptr - base);
+  return VLBM_OK;
+}
+
+int vlbm_ipc_open(const unsigned char handle[64], void** d_base) {
+  if (!handle || !d_base) return set_error(VLBM_E_INVALID, "ipc: null argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, 64);
+  CU(cudaIpcOpenMemHandle(d_base, h, cudaIpcMemLazyEnablePeerAccess));
+  return VLBM_OK;
+}
+
+int vlbm_ipc_close(void* d_base) {
+  CU(cudaIpcCloseMemHandle(d_base));
   return VLBM_OK;
 }
 

@@ -75,6 +75,10 @@ cudaError_t launch_w1_restrict(int M, int nxc, int nyc, const double* coarse,
                                int64_t f_sample_stride, double* terms, cudaStream_t st);
 cudaError_t launch_w1_cells(int M, int64_t n, const double* a, const double* b, double* terms,
                             cudaStream_t st);
+// row tables: sample m's coarse plane at a_rows[m], fine plane at f_rows[m]
+// (any GPU, peer-mapped), cells [cell0, cell0 + n) of the coarse grid
+cudaError_t launch_w1_rows(int M, int nxc, int64_t cell0, int64_t n, const double* const* a_rows,
+                           const double* const* f_rows, double* terms, cudaStream_t st);
 cudaError_t launch_ordered_mean(int64_t n, const double* terms, double* result, cudaStream_t st);
 // nq entries per sample: x(m, q) = x[m * sample_stride + q]
 cudaError_t launch_moments(int M, int64_t nq, const double* x, int64_t sample_stride,

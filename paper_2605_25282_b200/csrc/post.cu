@@ -377,7 +377,36 @@ __device__ __forceinline__ double w1_cell(int M, int lane, double* ca, const dou
 //            bs = fine sample stride; 32-byte coarse and two 64-byte fine
 //            segments per sample, every fetched sector fully used)
 //   kKind 2: cell-major columns after the sample->cell re-shard, a[c*M + m]
+//   kKind 3: row tables (peer memory): a, b are device arrays of M row
+//            pointers (const double* const*) -- sample m's coarse plane and
+//            fine plane, each on whichever GPU holds the sample (NVLink peer
+//            mapping); as = the first global cell of this launch; the
+//            restriction is fused as in kind 1
 constexpr int kW1Cells = 4;
+
+// Sample m's value pair of (launch-local) cell c for the W1 kernels.
+template <int kKind>
+__device__ __forceinline__ void w1_load(int M, long long c, int m, int nxc, const double* a,
+                                        long long as, const double* b, long long bs,
+                                        double& va, double& vb) {
+  if (kKind == 2) {
+    va = a[c * M + m];
+    vb = b[c * M + m];
+  } else if (kKind == 3) {
+    const long long cg = as + c;
+    const int j = (int)(cg / nxc), i = (int)(cg - (long long)j * nxc);
+    va = reinterpret_cast<const double* const*>(a)[m][cg];
+    vb = restrict_at(reinterpret_cast<const double* const*>(b)[m], 2 * nxc, i, j);
+  } else {
+    va = a[(long long)m * as + c];
+    if (kKind == 1) {
+      const int j = (int)(c / nxc), i = (int)(c - (long long)j * nxc);
+      vb = restrict_at(b + (long long)m * bs, 2 * nxc, i, j);
+    } else {
+      vb = b[(long long)m * bs + c];
+    }
+  }
+}
 
 template <int R, int kKind>
 __global__ void __launch_bounds__(32 * kW1Cells, 4) k_w1_tile(int M, long long n, int nxc,
@@ -401,20 +430,7 @@ __global__ void __launch_bounds__(32 * kW1Cells, 4) k_w1_tile(int M, long long n
     }
     const long long c = c0 + cl;
     double va = 0.0, vb = 0.0;
-    if (c < n) {
-      if (kKind == 2) {
-        va = a[c * M + m];
-        vb = b[c * M + m];
-      } else {
-        va = a[(long long)m * as + c];
-        if (kKind == 1) {
-          const int j = (int)(c / nxc), i = (int)(c - (long long)j * nxc);
-          vb = restrict_at(b + (long long)m * bs, 2 * nxc, i, j);
-        } else {
-          vb = b[(long long)m * bs + c];
-        }
-      }
-    }
+    if (c < n) w1_load<kKind>(M, c, m, nxc, a, as, b, bs, va, vb);
     sa[cl * LD + m] = va;
     sb[cl * LD + m] = vb;
   }
@@ -563,18 +579,10 @@ __global__ void k_w1_keys(int M, long long c0, long long nb, int nxc, const doub
     const long long cl = cb + tx, c = c0 + cl;
     unsigned long long va = 0, vb = 0;
     if (m < M && cl < nb) {
-      if (kKind == 2) {
-        va = dkey(a[c * M + m]);
-        vb = dkey(b[c * M + m]);
-      } else {
-        va = dkey(a[(long long)m * as + c]);
-        if (kKind == 1) {
-          const int j = (int)(c / nxc), i = (int)(c - (long long)j * nxc);
-          vb = dkey(restrict_at(b + (long long)m * bs, 2 * nxc, i, j));
-        } else {
-          vb = dkey(b[(long long)m * bs + c]);
-        }
-      }
+      double x, y;
+      w1_load<kKind>(M, c, m, nxc, a, as, b, bs, x, y);
+      va = dkey(x);
+      vb = dkey(y);
     }
     ta[r][tx] = va;
     tb[r][tx] = vb;
@@ -700,6 +708,12 @@ cudaError_t launch_w1_restrict(int M, int nxc, int nyc, const double* a, int64_t
 cudaError_t launch_w1_cells(int M, int64_t n, const double* a, const double* b, double* terms,
                             cudaStream_t st) {
   return launch_w1<2>(M, n, 0, a, 0, b, 0, terms, st);
+}
+
+cudaError_t launch_w1_rows(int M, int nxc, int64_t cell0, int64_t n, const double* const* a_rows,
+                           const double* const* f_rows, double* terms, cudaStream_t st) {
+  return launch_w1<3>(M, n, nxc, reinterpret_cast<const double*>(a_rows), cell0,
+                      reinterpret_cast<const double*>(f_rows), 0, terms, st);
 }
 
 cudaError_t launch_ordered_mean(int64_t n, const double* terms, double* result, cudaStream_t st) {

@@ -13,6 +13,11 @@ GPU, torch.distributed over NCCL (gloo on CPU for the tests).
   wasserstein1 (metrics.hpp:112-124).  strong_error's per-sample partials are
   gathered in sample order the same way (metrics.hpp:63-89).
 
+``peer_wasserstein1`` is the fused alternative to the all_to_all: each
+rank's W1 kernel reads the other ranks' sample planes directly from their
+memory (CUDA IPC peer mappings over NVLink) while it sorts, so the
+transfer overlaps the compute and no re-sharded copy is materialised.
+
 Everything here is data movement; the arithmetic runs in the CUDA kernels
 (``term_fn`` / ``mean_fn`` arguments default to the device implementations).
 """
@@ -112,6 +117,119 @@ def distributed_wasserstein1(torch, dist, coarse_local, restricted_local, valid_
     if allterms is None:
         return None
     return mean_fn(allterms)
+
+
+_IPC_MAPS: dict = {}  # handle bytes -> [base pointer, open count] (one map per process)
+
+
+def _ipc_open(L, C, v, hb: bytes) -> int:
+    ent = _IPC_MAPS.get(hb)
+    if ent is None:
+        ptr = C.c_void_p()
+        v._check(L.vlbm_ipc_open((C.c_ubyte * 64).from_buffer_copy(hb), C.byref(ptr)))
+        ent = _IPC_MAPS[hb] = [ptr.value, 0]
+    ent[1] += 1
+    return ent[0]
+
+
+def _ipc_close(L, v, hb: bytes) -> None:
+    ent = _IPC_MAPS[hb]
+    ent[1] -= 1
+    if ent[1] == 0:
+        del _IPC_MAPS[hb]
+        v._check(L.vlbm_ipc_close(ent[0]))
+
+
+class PeerRows:
+    """Row tables of a sample-sharded ensemble in peer memory: every rank
+    exports its planes' allocations with CUDA IPC (vlbm_ipc_handle), the
+    handles travel with one all_gather_object, and every rank maps the
+    others' allocations (vlbm_ipc_open, peer access over NVLink).  ``rows``
+    then lists one device pointer per sample of the whole ensemble in global
+    order, wherever the sample lives.  Use as a context manager: leaving it
+    barriers (no rank unmaps memory a peer may still read) and unmaps."""
+
+    def __init__(self, torch, dist, planes_local, sample_bytes: int, group=None):
+        import ctypes as C
+
+        from . import vlbm as v
+        self.torch, self.dist, self.group = torch, dist, group
+        self.L, self.C, self.v = v.lib(), C, v
+        self.rank = dist.get_rank(group)
+        self.opened = []
+        h = (C.c_ubyte * 64)()
+        off = C.c_uint64()
+        m_local = planes_local.shape[0]
+        if m_local:
+            v._check(self.L.vlbm_ipc_handle(planes_local.data_ptr(), h, C.byref(off)))
+        mine = (bytes(h), int(off.value), m_local, torch.cuda.current_device())
+        world = dist.get_world_size(group)
+        allh = [None] * world
+        dist.all_gather_object(allh, mine, group=group)
+        self.rows = []
+        for q, (hb, offset, mq, dev) in enumerate(allh):
+            if mq == 0:
+                continue
+            if q == self.rank:
+                base = planes_local.data_ptr()
+            else:
+                base = _ipc_open(self.L, C, v, hb) + offset
+                self.opened.append(hb)
+            self.rows.extend(base + k * sample_bytes for k in range(mq))
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.torch.cuda.synchronize()
+        self.dist.barrier(group=self.group)  # every peer is done reading
+        for hb in self.opened:
+            _ipc_close(self.L, self.v, hb)
+        self.opened = []
+
+
+def peer_wasserstein1(torch, dist, coarse_local, fine_local, valid_local, nxc: int,
+                      group=None):
+    """wasserstein1(coarse, restrict_field(fine)) of one variable over the
+    jointly valid samples of a sample-sharded ensemble pair, with NO
+    re-shard: each rank computes the terms of its contiguous cell range in
+    one kernel that reads every sample's coarse and fine planes where they
+    live (vlbm_d_w1_rows over CUDA-IPC peer mappings), so the NVLink
+    transfer overlaps the sort; then the per-cell terms go to rank 0 in
+    storage order for the sequential mean (bit-identical to the single-
+    process wasserstein1).  coarse_local: [m_local, nyc * nxc] float64,
+    fine_local: [m_local, 4 * nyc * nxc] (unrestricted), valid_local: bool
+    [m_local].  Returns W1 on rank 0, None elsewhere."""
+    from . import vlbm as v
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    m_local, nc = coarse_local.shape
+    if fine_local.shape != (m_local, 4 * nc):
+        raise ValueError("wasserstein1: inconsistent field sizes")
+    coarse_local, fine_local = coarse_local.contiguous(), fine_local.contiguous()
+    vmask = [None] * world
+    dist.all_gather_object(vmask, [bool(x) for x in valid_local.tolist()], group=group)
+    keep = [k for vm in vmask for k in vm]
+    M = sum(keep)
+    if M < 1:
+        raise RuntimeError("metrics: no jointly valid samples for pair")
+    dev = coarse_local.device
+    with PeerRows(torch, dist, coarse_local, 8 * nc, group) as cr, \
+            PeerRows(torch, dist, fine_local, 32 * nc, group) as fr:
+        sel = [i for i, k in enumerate(keep) if k]
+        a_rows = torch.tensor([cr.rows[i] for i in sel], dtype=torch.int64, device=dev)
+        f_rows = torch.tensor([fr.rows[i] for i in sel], dtype=torch.int64, device=dev)
+        c0, cn = shard_range(nc, world, rank)
+        terms = torch.empty(cn, dtype=torch.float64, device=dev)
+        v._check(v.lib().vlbm_d_w1_rows(M, nxc, c0, cn, a_rows.data_ptr(), f_rows.data_ptr(),
+                                        terms.data_ptr(),
+                                        torch.cuda.current_stream(dev).cuda_stream))
+        if dist.get_backend(group) == "gloo":  # host gather (tests: ranks sharing a GPU)
+            terms = terms.cpu()
+        allterms = ordered_gather(torch, dist, terms, group)
+    if allterms is None:
+        return None
+    return _device_mean(torch, allterms.to(dev))
 
 
 def distributed_strong_error(torch, dist, partials_local, group=None,

@@ -89,3 +89,4 @@ def test_bench_sharded_postproc_matches_single_device(nccl_group):
     fine.normal_(-0.125, 0.5, generator=gen).exp_()
     assert float(r["W1"]).hex() == float(post.wasserstein1(torch, coarse, fine)).hex()
     assert r["w1_cells_per_s"] > 0
+    assert r["peer"]["identical"] and r["peer"]["w1_cells_per_s"] > 0
