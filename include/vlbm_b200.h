@@ -180,6 +180,9 @@ int vlbm_batch_get(vlbm_batch* b, int s, double* u, double* pops, double* time, 
                    int* status);
 /* All samples' u into n_samples field blocks (snapshot of the batch). */
 int vlbm_batch_get_fields(vlbm_batch* b, double* u_all);
+/* The same dense (S x 4 x ny x nx) fields into DEVICE memory of the batch's
+ * GPU (snapshots kept on the device for the on-device metrics; no host copy). */
+int vlbm_batch_copy_fields_device(vlbm_batch* b, double* d_u_all);
 /* Per-sample scalars: time, steps, status (arrays of n_samples; any NULL). */
 int vlbm_batch_get_scalars(vlbm_batch* b, double* time, int64_t* steps, int* status);
 /* Cell theta (ny x nx) of sample s from the last limiter pass. */

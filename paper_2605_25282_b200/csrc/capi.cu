@@ -568,6 +568,24 @@ int vlbm_batch_get_fields(vlbm_batch* b, double* u_all) {
   return VLBM_OK;
 }
 
+int vlbm_batch_copy_fields_device(vlbm_batch* b, double* d_u_all) {
+  if (!b || !d_u_all) return set_error(VLBM_E_INVALID, "null argument");
+  CU(cudaSetDevice(b->device));
+  std::vector<SampleCtl> ctl;
+  if (int rc = read_ctl(b, ctl)) return rc;
+  const MarchParams& P = b->P;
+  const size_t n = (size_t)P.nx * P.ny;
+  for (int s = 0; s < b->S; ++s) {
+    const double* src = (ctl[s].parity ? P.buf1 : P.buf0) + (size_t)s * P.sample_stride;
+    for (int k = 0; k < 4; ++k)
+      CU(cudaMemcpy2DAsync(d_u_all + (4 * (size_t)s + k) * n, sizeof(double) * P.nx,
+                           src + k * P.plane, sizeof(double) * P.pitch, sizeof(double) * P.nx,
+                           P.ny, cudaMemcpyDeviceToDevice, b->stream));
+  }
+  CU(cudaStreamSynchronize(b->stream));
+  return VLBM_OK;
+}
+
 int vlbm_batch_get_scalars(vlbm_batch* b, double* time, int64_t* steps, int* status) {
   if (!b) return set_error(VLBM_E_INVALID, "null batch");
   CU(cudaSetDevice(b->device));

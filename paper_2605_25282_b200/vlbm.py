@@ -176,6 +176,7 @@ def lib() -> C.CDLL:
     sig("vlbm_batch_step_with_blending", I, [V, D, DP, DP])
     sig("vlbm_batch_get", I, [V, I, DP, DP, DP, C.POINTER(I64), C.POINTER(I)])
     sig("vlbm_batch_get_fields", I, [V, DP])
+    sig("vlbm_batch_copy_fields_device", I, [V, V])
     sig("vlbm_batch_get_scalars", I, [V, DP, C.POINTER(I64), C.POINTER(I)])
     sig("vlbm_batch_get_theta", I, [V, I, DP])
     sig("vlbm_batch_device_u", I, [V, I, C.POINTER(DP)])
@@ -354,6 +355,10 @@ class BatchSimulation:
         u = np.zeros((self.n, 4, self.grid.ny, self.grid.nx))
         _check(lib().vlbm_batch_get_fields(self._h, _dp(u)))
         return u
+
+    def fields_to_device(self, ptr: int) -> None:
+        """Dense (n, 4, ny, nx) fields into device memory at ptr (same GPU)."""
+        _check(lib().vlbm_batch_copy_fields_device(self._h, ptr))
 
     def scalars(self):
         t = np.zeros(self.n)
