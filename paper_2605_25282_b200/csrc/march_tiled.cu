@@ -555,9 +555,11 @@ __global__ void __launch_bounds__(256, 2) k_theta_hard(MarchParams P) {
     if (cls == 1) my = atomicAdd(&nb, 1);
     if (cls == 2) my = atomicAdd(&nc[ccls], 1);
     __syncthreads();
-    if (threadIdx.x == 0) {
-      baseb = nb ? atomicAdd(P.hq_n + 2, nb) : 0;
-      for (int k = 0; k < 3; ++k) basec[k] = nc[k] ? atomicAdd(P.hq_n + 3 + k, nc[k]) : 0;
+    // the four queue reservations by four warps' first lanes, in parallel
+    if (threadIdx.x == 0) baseb = nb ? atomicAdd(P.hq_n + 2, nb) : 0;
+    if (threadIdx.x >= 32 && threadIdx.x < 128 && (threadIdx.x & 31) == 0) {
+      const int k = (threadIdx.x >> 5) - 1;
+      basec[k] = nc[k] ? atomicAdd(P.hq_n + 3 + k, nc[k]) : 0;
     }
     __syncthreads();
     const int third = P.hq_cap / 3;
