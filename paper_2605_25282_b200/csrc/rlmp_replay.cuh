@@ -60,30 +60,48 @@ __device__ __forceinline__ double vertex_p(const cs& fo, const cs* cf, int S, do
   return pressure(vertex_at(fo, t, S), gm1);
 }
 
+// Reciprocal to ~1e-15 relative without the IEEE division's correction step
+// and slow-path check (MUFU.RCP64H + two Newton steps): for the crossing
+// estimates and band widths, which only place test points, and for bounds
+// that carry a larger relative slack.
+__device__ __forceinline__ double arcp(double x) {
+#ifdef __CUDA_ARCH__
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+#else
+  return 1.0 / x;
+#endif
+}
+
 // Estimated crossings th > 0 of p(u_FO + th d) = c (ascending; returns the
 // count).  Uses p / (gamma-1) = A_w(u) - |m - w rho|^2 / 2 rho with w the
 // velocity of u_FO, which keeps the cancellation of the jet core out of the
 // coefficients:  (D + th A1)(rho0 + th d.r) - th^2 Q = 0.
 __device__ __forceinline__ int crossings(const cs& fo, double p0, const cs& d, double c,
                                          double gm1, double* r, double* slope) {
-  const double wx = fo.mx / fo.r, wy = fo.my / fo.r;
+  const double rinv = arcp(fo.r);
+  const double wx = fo.mx * rinv, wy = fo.my * rinv;
   const double A1 = (d.e - (wx * d.mx + wy * d.my)) + 0.5 * (wx * wx + wy * wy) * d.r;
   const double qx = d.mx - wx * d.r, qy = d.my - wy * d.r;
   const double Q = 0.5 * (qx * qx + qy * qy);
-  const double D = (p0 - c) / gm1;
+  const double D = (p0 - c) * arcp(gm1);
   const double a2 = A1 * d.r - Q, a1 = D * d.r + A1 * fo.r, a0 = D * fo.r;
   double x0, x1;
   if (a2 == 0.0) {
     if (a1 == 0.0) return 0;
-    x0 = x1 = -a0 / a1;
+    x0 = x1 = -a0 * arcp(a1);
   } else {
     const double disc = a1 * a1 - 4.0 * a2 * a0;
     if (!(disc >= 0.0)) return 0;
     const double s = sqrt(disc);
     const double q = -0.5 * (a1 + (a1 < 0.0 ? -s : s));
     if (q == 0.0) return 0;
-    x0 = q / a2;
-    x1 = a0 / q;
+    x0 = q * arcp(a2);
+    x1 = a0 * arcp(q);
     if (x1 < x0) {
       const double t = x0;
       x0 = x1;
@@ -95,7 +113,7 @@ __device__ __forceinline__ int crossings(const cs& fo, double p0, const cs& d, d
   if (x1 > 0.0 && isfinite(x1) && x1 != x0) r[n++] = x1;
   // |dp/dth| at the crossings: (gamma-1) |h'(x)| / rho(x)
   for (int k = 0; k < n; ++k)
-    slope[k] = gm1 * fabs(2.0 * a2 * r[k] + a1) / fabs(fo.r + r[k] * d.r);
+    slope[k] = gm1 * fabs(2.0 * a2 * r[k] + a1) * arcp(fabs(fo.r + r[k] * d.r));
   return n;
 }
 
@@ -123,7 +141,7 @@ __device__ __forceinline__ RayCls classify_ge(const cs& fo, const cs& d, double 
     return k;
   }
   const double x = r[0];
-  double w = band0(x, thc) + 5.0 * err / sl[0];
+  double w = band0(x, thc) + 5.0 * err * arcp(sl[0]);
   if (!(w < thc)) return k;
   bool tdone = false, fdone = !(x + w < thc);
   for (int tr = 0; tr < 3 && !(tdone && fdone); ++tr, w *= 16.0) {
@@ -159,19 +177,20 @@ __device__ __forceinline__ RayCls classify_le_diag(const cs& fo, const cs& delta
   // Tangent bound: for any w, p/(gamma-1) = A_w(u) - |m - w rho|^2 / 2 rho
   // <= A_w(u), affine in th: A_w(u_FO) + th A_w(delta), and A_w(u_FO) =
   // p(u_FO)/(gamma-1) + |m_FO - w rho_FO|^2 / 2 rho_FO.
-  const double wx = fo.mx / fo.r, wy = fo.my / fo.r;
+  const double rinv = arcp(fo.r);  // any w works in the identity below
+  const double wx = fo.mx * rinv, wy = fo.my * rinv;
   const double ax = fabs(wx), ay = fabs(wy), kk = 0.5 * (wx * wx + wy * wy);
   const double A1 = (delta.e - (wx * delta.mx + wy * delta.my)) + kk * delta.r;
   const double eA = 8.0 * u * (((fabs(delta.e) + ax * fabs(delta.mx)) + ay * fabs(delta.my)) +
                                kk * fabs(delta.r));
   const double w0x = fabs(fo.mx - wx * fo.r) + 3.0 * u * (fabs(fo.mx) + ax * fo.r);
   const double w0y = fabs(fo.my - wy * fo.r) + 3.0 * u * (fabs(fo.my) + ay * fo.r);
-  const double lift = 1.01 * gm1 * (w0x * w0x + w0y * w0y) / (2.0 * fo.r);
+  const double lift = 1.01 * gm1 * (w0x * w0x + w0y * w0y) * arcp(2.0 * fo.r);
   const double base = (P0 + 2.01 * err) + lift;
   const double m = (c - base) - 4.0 * u * (fabs(c) + fabs(base));
   if (m > 0.0) {
     const double s = 1.01 * gm1 * (A1 + eA);
-    k.t1 = s <= 0.0 ? thc : 0.999999 * (m / s);
+    k.t1 = s <= 0.0 ? thc : 0.999999 * (m * arcp(s));
     if (!(k.t1 >= 0.0)) k.t1 = -1.0;
     if (k.t1 >= thc) return k;
   }
@@ -179,7 +198,7 @@ __device__ __forceinline__ RayCls classify_le_diag(const cs& fo, const cs& delta
   const int n = crossings(fo, P0, delta, c, gm1, r, sl);
   if (n == 0 || !(r[0] < thc)) return k;
   const double x1 = r[0], x2 = n > 1 ? r[1] : kInf;
-  const double w = band0(x1, thc) + 5.0 * err / (n > 1 ? smin(sl[0], sl[1]) : sl[0]);
+  const double w = band0(x1, thc) + 5.0 * err * arcp(n > 1 ? smin(sl[0], sl[1]) : sl[0]);
   if (!(w < thc)) return k;
   const double y1 = x1 + w, y2 = smin(x2 - w, thc);
   if (!(y1 <= y2)) return k;
