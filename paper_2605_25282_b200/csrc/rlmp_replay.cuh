@@ -60,23 +60,6 @@ __device__ __forceinline__ double vertex_p(const cs& fo, const cs* cf, int S, do
   return pressure(vertex_at(fo, t, S), gm1);
 }
 
-// Reciprocal to ~1e-15 relative without the IEEE division's correction step
-// and slow-path check (MUFU.RCP64H + two Newton steps): for the crossing
-// estimates and band widths, which only place test points, and for bounds
-// that carry a larger relative slack.
-__device__ __forceinline__ double arcp(double x) {
-#ifdef __CUDA_ARCH__
-  double y;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double e = fma(-x, y, 1.0);
-  y = fma(y, e, y);
-  e = fma(-x, y, 1.0);
-  return fma(y, e, y);
-#else
-  return 1.0 / x;
-#endif
-}
-
 // Estimated crossings th > 0 of p(u_FO + th d) = c (ascending; returns the
 // count).  Uses p / (gamma-1) = A_w(u) - |m - w rho|^2 / 2 rho with w the
 // velocity of u_FO, which keeps the cancellation of the jet core out of the
