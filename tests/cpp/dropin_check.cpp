@@ -13,8 +13,13 @@
 //   dropin_check outputs <dir>      metrics / rates CSVs (write_metrics_csv) and
 //                                   rendered PPMs (cmd_render vs gpu::render:
 //                                   mean, std, sample; rho, energy) byte-identical
+//   dropin_check acceptance <dir>   the reference's acceptance criteria 6-9 with
+//                                   the GPU drop-ins (reference's output format)
+#include <cmath>
+#include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <filesystem>
 #include <fstream>
 #include <map>
@@ -184,6 +189,129 @@ static int check_outputs(const fs::path& dir) {
   return bad ? 1 : 0;
 }
 
+// The reference's acceptance criteria 6-9 (tests/acceptance.cpp:251-402)
+// re-run with the GPU drop-ins in place of run_sample / run_ensemble /
+// compute_metrics; the lines are printed in the reference's own format so
+// they can be compared with its recorded results (tests/golden/acceptance.json).
+static void accept_report(int number, const std::string& label, bool pass,
+                          const std::string& detail) {
+  std::printf("criterion %2d %-28s %s  (%s)\n", number, label.c_str(), pass ? "PASS" : "FAIL",
+              detail.c_str());
+}
+
+static std::string afmt(const char* f, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, f);
+  std::vsnprintf(buf, sizeof(buf), f, ap);
+  va_end(ap);
+  return buf;
+}
+
+static int check_acceptance(const fs::path& dir) {
+  {  // criterion 6: jet-head velocity of the unperturbed jet (acceptance.cpp:251-281)
+    PerturbationParams pp;
+    pp.amplitude = 0.0;
+    SampleSpec spec;
+    spec.grid = Grid{500, 100};
+    spec.gas = GasParams{5.0 / 3.0};
+    spec.perturbation = pp;
+    spec.coeffs = draw_coefficients(42, 0, pp.modes);
+    spec.snapshot_times = {0.001, 0.0015, 0.002, 0.0025, 0.003};
+    const SampleResult res = gpu::run_samples({spec})[0];
+    std::vector<double> ts, xs;
+    for (const FieldSnapshot& sn : res.snapshots) {
+      ts.push_back(sn.time);
+      xs.push_back(jet_head_position(sn, pp.rho_amb, pp.r_jet, 2.0));
+    }
+    const double v = fit_slope(ts, xs);
+    accept_report(6, "jet-head velocity", res.admissible && std::abs(v - 666.7) <= 0.10 * 666.7,
+                  afmt("fitted head speed %.1f over t in [0.001,0.003], want 666.7 +/- 10%%", v));
+  }
+  CaseConfig cfg;  // the 64-sample, three-grid desk case (acceptance.cpp:285-293)
+  cfg.output_dir = (dir / "accept").string();
+  const EnsembleManifest man = gpu::run_ensemble(cfg);
+  {  // criterion 7 (acceptance.cpp:295-317)
+    const MetricsReport rep = gpu::compute_metrics(man);
+    double r_w1_end = NAN, r_s_end = NAN, r_w1_0 = NAN, r_s_0 = NAN;
+    for (const RateRow& r : rep.rates) {
+      if (std::abs(r.time - man.config.t_end) < 1e-12) r_w1_end = r.r_w1, r_s_end = r.r_strong;
+      if (r.time == 0.0) r_w1_0 = r.r_w1, r_s_0 = r.r_strong;
+    }
+    auto in = [](double v, double lo, double hi) { return v >= lo && v <= hi; };
+    const bool pass = (r_w1_end - r_s_end) >= 0.2 && r_s_end <= 0.2 && in(r_w1_0, 0.8, 1.2) &&
+                      in(r_s_0, 0.8, 1.2);
+    accept_report(7, "statistical rate separation", pass,
+                  afmt("t=end: r_W1 %.3f, r_strong %.3f (need gap >= 0.2, r_strong <= 0.2); "
+                       "t=0: %.3f/%.3f (need [0.8,1.2])",
+                       r_w1_end, r_s_end, r_w1_0, r_s_0));
+  }
+  {  // criterion 8: determinism and resume (acceptance.cpp:358-402), one sample per batch
+    CaseConfig c8;
+    c8.grids = {{40, 8}, {80, 16}};
+    c8.samples = 4;
+    c8.t_end = 0.0005;
+    c8.snapshot_times = {0.0, 0.00025, 0.0005};
+    const fs::path root = dir / "det";
+    c8.output_dir = (root / "run").string();
+    auto execute = [&](const std::function<bool()>& stop) {
+      const EnsembleManifest m = gpu::run_ensemble(c8, {}, stop, 0, 1);
+      bool complete = true;
+      for (const SampleRecord& r : m.samples)
+        for (RunStatus st : r.status)
+          if (st == RunStatus::NotRun) complete = false;
+      if (complete) {
+        const MetricsReport rep = gpu::compute_metrics(m);
+        write_metrics_csv(rep, m.root / "metrics.csv", m.root / "rates.csv");
+      }
+    };
+    fs::remove_all(root);
+    execute({});
+    const auto first = dir_bytes(c8.output_dir);
+    fs::remove_all(root);
+    execute({});
+    const bool rerun_same = dir_bytes(c8.output_dir) == first;
+    fs::remove_all(root);
+    int done = 0;
+    execute([&done] { return ++done > 3; });
+    const bool was_partial = dir_bytes(c8.output_dir) != first;
+    execute({});
+    const bool resume_same = dir_bytes(c8.output_dir) == first;
+    accept_report(8, "determinism and resume", rerun_same && was_partial && resume_same,
+                  afmt("rerun identical: %s; interrupted run partial: %s; resumed identical: %s",
+                       rerun_same ? "yes" : "no", was_partial ? "yes" : "no",
+                       resume_same ? "yes" : "no"));
+  }
+  {  // criterion 9 (acceptance.cpp:319-352)
+    const double eps = 1e-7;
+    const GasParams gas = man.config.gas;
+    const double rho_floor = eps * man.config.perturbation.rho_amb;
+    const double p_floor = eps * man.config.perturbation.p_amb;
+    double min_rho = INFINITY, min_p = INFINITY;
+    int admissible = 0, diverged = 0;
+    for (std::size_t gi = 0; gi < man.config.grids.size(); ++gi) {
+      for (std::size_t m = 0; m < man.samples.size(); ++m) {
+        if (man.samples[m].status[gi] == RunStatus::Diverged) {
+          ++diverged;
+          continue;
+        }
+        ++admissible;
+        for (const FieldSnapshot& sn : load_sample_snapshots(man, gi, static_cast<int>(m))) {
+          for (const ConservedState& u : sn.data) {
+            min_rho = std::min(min_rho, u.rho);
+            min_p = std::min(min_p, pressure(u, gas));
+          }
+        }
+      }
+    }
+    accept_report(9, "positivity across ensemble", min_rho >= rho_floor && min_p >= p_floor,
+                  afmt("min rho %.3e (floor %.3e), min p %.3e (floor %.3e); %d admissible, "
+                       "%d diverged runs all recorded",
+                       min_rho, rho_floor, min_p, p_floor, admissible, diverged));
+  }
+  return 0;
+}
+
 int main(int argc, char** argv) {
   if (argc < 2) return 2;
   const std::string mode = argv[1];
@@ -193,6 +321,7 @@ int main(int argc, char** argv) {
     if (mode == "ensemble" && argc >= 3) return check_ensemble(argv[2], argc > 3 ? std::atoi(argv[3]) : 8);
     if (mode == "metrics" && argc >= 3) return check_metrics(argv[2]);
     if (mode == "outputs" && argc >= 3) return check_outputs(argv[2]);
+    if (mode == "acceptance" && argc >= 3) return check_acceptance(argv[2]);
   } catch (const std::exception& e) {
     std::printf("exception: %s\n", e.what());
     return 3;

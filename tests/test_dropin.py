@@ -65,3 +65,32 @@ def test_gpu_run_ensemble_byte_identical_to_reference_and_metrics():
         assert rc == 0 and "renders:" in out, out
     finally:
         shutil.rmtree(d, ignore_errors=True)
+
+
+@pytest.mark.gpu
+def test_reference_acceptance_criteria_6_to_9_on_gpu():
+    """The reference's own acceptance gate (tests/acceptance.cpp criteria 6-9:
+    jet-head velocity, rate separation of the 64-sample three-grid ensemble,
+    determinism and resume, positivity) re-run with the GPU drop-ins; every
+    result line equals the one the reference recorded for its CPU run
+    (tests/golden/acceptance.json from proj/test_output.txt) -- including
+    criterion 7's FAIL, which is the reference's result at desk scale."""
+    import json
+    if not os.path.exists(BIN):
+        pytest.skip("dropin_check not built")
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "acceptance.json")))
+    d = tempfile.mkdtemp(prefix="vlbm_accept_")
+    try:
+        rc, out = _run("acceptance", d)
+    finally:
+        shutil.rmtree(d, ignore_errors=True)
+    assert rc == 0, out
+    got = {}
+    for line in out.splitlines():
+        if line.startswith("criterion"):
+            num = line.split()[1]
+            head, _, detail = line.partition("  (")
+            got[num] = {"verdict": head.split()[-1], "detail": detail[:-1]}
+    for num, want in gold["criteria"].items():
+        assert got[num]["verdict"] == want["verdict"], (num, got[num], want)
+        assert got[num]["detail"] == want["detail"], (num, got[num], want)
