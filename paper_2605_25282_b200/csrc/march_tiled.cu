@@ -74,13 +74,17 @@ __device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned
                "r"(bytes)
                : "memory");
 }
+// try_wait with a suspend-time hint: a waiting warp is parked by the
+// hardware until the phase completes (or the hint expires) instead of
+// spinning, so warps that reach the next tile early do not take issue slots
+// from the warps still finishing this one.
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
   asm volatile(
       "{\n .reg .pred p;\n"
       "WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
       " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-      "r"(phase)
+      "r"(phase), "r"(0x989680)
       : "memory");
 }
 // 4-D tile [x, y, plane, sample] -> shared memory, OOB elements zero-filled.
