@@ -197,7 +197,18 @@ def postproc_bench(torch, dev, M=1000, nxc=2000, nyc=400, reps=3):
         l1_ms.append(ev[2].elapsed_time(ev[3]))
     w1 = float(res.item())
     es = post.strong_finish(part.cpu().numpy())
-    w1t = statistics.median(w1_ms) + statistics.median(mean_ms)
+    # the production call: terms and the storage-order mean overlapped
+    wm = torch.empty(2, dtype=torch.float64, device=coarse.device)
+    post.w1_mean(torch, coarse, fine, wm, terms)
+    fused_ms = []
+    for _ in range(reps):
+        ev[0].record()
+        post.w1_mean(torch, coarse, fine, wm, terms)
+        ev[1].record()
+        torch.cuda.synchronize()
+        fused_ms.append(ev[0].elapsed_time(ev[1]))
+    assert float(wm[0].item()) == w1, "overlapped W1 differs from terms + ordered mean"
+    w1t = statistics.median(fused_ms)
     l1t = statistics.median(l1_ms)
     hbm, src = peaks()
     w1_bytes = 40.0 * M * nc  # M coarse + 4M fine values per coarse cell
@@ -209,6 +220,8 @@ def postproc_bench(torch, dev, M=1000, nxc=2000, nyc=400, reps=3):
                     f"fine {2 * nxc}x{2 * nyc}",
         "w1_cells_per_s": nc / (w1t * 1e-3), "w1_ms": w1t,
         "w1_kernel_ms": statistics.median(w1_ms), "ordered_mean_ms": statistics.median(mean_ms),
+        "w1_note": "w1_ms: vlbm_d_w1_restrict_mean (the mean overlapped with the terms); "
+                   "w1_kernel_ms + ordered_mean_ms: the two phases run back to back",
         "w1_values_sorted_per_s": 2 * M * nc / (statistics.median(w1_ms) * 1e-3),
         "w1_roofline": {"bound": "hbm", "achieved": w1_bytes / (statistics.median(w1_ms) * 1e-3)
                         / 1e9, "peak": hbm, "unit": "GB/s",

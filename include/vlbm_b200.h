@@ -255,6 +255,14 @@ int vlbm_strong_finish(int M, const double* partials, double* result, double* pe
 int vlbm_d_w1_restrict(int M, int nxc, int nyc, const double* d_coarse, int64_t c_stride,
                        const double* d_fine, int64_t f_stride, double* d_cell_terms,
                        void* stream);
+/* vlbm_d_w1_restrict + vlbm_d_ordered_mean in one call, the storage-order
+ * mean overlapped with the per-cell terms (cells in chunks of whole coarse
+ * rows; each chunk's part of the sequential sum runs on an internal stream
+ * once its terms exist).  d_terms: n_cells doubles, d_scratch: 1 double,
+ * d_result: W1 (wasserstein1's return value, bit-identical). */
+int vlbm_d_w1_restrict_mean(int M, int nxc, int nyc, const double* d_coarse, int64_t c_stride,
+                            const double* d_fine, int64_t f_stride, double* d_terms,
+                            double* d_scratch, double* d_result, void* stream);
 /* Restricted-fine plane of one variable into a (M x n_cells) array. */
 int vlbm_d_restrict_var(int M, int nxc, int nyc, const double* d_fine, int var, double* d_out,
                         void* stream);

@@ -809,6 +809,16 @@ int vlbm_d_w1_restrict(int M, int nxc, int nyc, const double* d_coarse, int64_t 
   return VLBM_OK;
 }
 
+int vlbm_d_w1_restrict_mean(int M, int nxc, int nyc, const double* d_coarse, int64_t c_stride,
+                            const double* d_fine, int64_t f_stride, double* d_terms,
+                            double* d_scratch, double* d_result, void* stream) {
+  if (M < 1) return set_error(VLBM_E_INVALID, "wasserstein1: sample counts differ or are empty");
+  if (nxc < 1 || nyc < 1) return set_error(VLBM_E_INVALID, "wasserstein1: empty grid");
+  CU(vlbm_impl::launch_w1_restrict_mean(M, nxc, nyc, d_coarse, c_stride, d_fine, f_stride, d_terms,
+                                        d_scratch, d_result, (cudaStream_t)stream));
+  return VLBM_OK;
+}
+
 int vlbm_d_restrict_var(int M, int nxc, int nyc, const double* d_fine, int var, double* d_out,
                         void* stream) {
   CU(vlbm_impl::launch_restrict_var(M, nxc, nyc, d_fine, var, d_out, (cudaStream_t)stream));

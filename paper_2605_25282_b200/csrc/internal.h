@@ -80,6 +80,12 @@ cudaError_t launch_w1_cells(int M, int64_t n, const double* a, const double* b, 
 cudaError_t launch_w1_rows(int M, int nxc, int64_t cell0, int64_t n, const double* const* a_rows,
                            const double* const* f_rows, double* terms, cudaStream_t st);
 cudaError_t launch_ordered_mean(int64_t n, const double* terms, double* result, cudaStream_t st);
+// W1 (fused restriction) with the storage-order mean overlapped chunk by chunk
+// on an internal stream; terms: n cells, acc: one device double of scratch
+cudaError_t launch_w1_restrict_mean(int M, int nxc, int nyc, const double* coarse,
+                                    int64_t c_sample_stride, const double* fine,
+                                    int64_t f_sample_stride, double* terms, double* acc,
+                                    double* result, cudaStream_t st);
 // nq entries per sample: x(m, q) = x[m * sample_stride + q]
 cudaError_t launch_moments(int M, int64_t nq, const double* x, int64_t sample_stride,
                            double* mean, double* stddev, cudaStream_t st);

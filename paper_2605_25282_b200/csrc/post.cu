@@ -444,8 +444,12 @@ __global__ void __launch_bounds__(32 * kW1Cells, 4) k_w1_tile(int M, long long n
 
 // acc = sum_c terms[c] in storage order; result = acc / n (metrics.hpp:112-124).
 constexpr int kOmChunk = 2048;
-__global__ void __launch_bounds__(256) k_ordered_mean(long long n, const double* terms,
-                                                     double* result) {
+// acc continues from *acc_io unless first; writes acc back to *acc_io (if
+// given) and acc / n_total to *result (if given): a storage-order sum can be
+// run in pieces, each piece continuing the previous one's chain exactly.
+__global__ void __launch_bounds__(256) k_ordered_sum(long long n, const double* terms,
+                                                    double* acc_io, int first, long long n_total,
+                                                    double* result) {
   __shared__ __align__(16) double buf[2][kOmChunk];
   const long long nchunks = (n + kOmChunk - 1) / kOmChunk;
   auto stage = [&](long long ch, int bi, int t0, int nt) {
@@ -455,7 +459,7 @@ __global__ void __launch_bounds__(256) k_ordered_mean(long long n, const double*
   };
   stage(0, 0, threadIdx.x, blockDim.x);
   __syncthreads();
-  double acc = 0.0;
+  double acc = first ? 0.0 : *acc_io;
   for (long long ch = 0; ch < nchunks; ++ch) {
     const int bi = (int)(ch & 1);
     if (threadIdx.x >= 32) {
@@ -489,7 +493,10 @@ __global__ void __launch_bounds__(256) k_ordered_mean(long long n, const double*
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) *result = acc / static_cast<double>(n);
+  if (threadIdx.x == 0) {
+    if (acc_io) *acc_io = acc;
+    if (result) *result = acc / static_cast<double>(n_total);
+  }
 }
 
 // ensemble_moments per (component, cell) on sample-major blocks: x(m, q) =
@@ -717,8 +724,47 @@ cudaError_t launch_w1_rows(int M, int nxc, int64_t cell0, int64_t n, const doubl
 }
 
 cudaError_t launch_ordered_mean(int64_t n, const double* terms, double* result, cudaStream_t st) {
-  k_ordered_mean<<<1, 256, 0, st>>>(n, terms, result);
+  k_ordered_sum<<<1, 256, 0, st>>>(n, terms, nullptr, 1, n, result);
   return cudaGetLastError();
+}
+
+// W1 of coarse planes vs the restricted fine planes with the storage-order
+// mean overlapped: the cells are processed in K chunks of whole coarse rows
+// on `st`; each chunk's part of the sequential sum runs on a second stream
+// as soon as its terms exist, continuing the chain of the previous chunk
+// (the same additions in the same order), so only the last chunk's part of
+// the chain follows the last W1 launch.  result: device scalar.
+cudaError_t launch_w1_restrict_mean(int M, int nxc, int nyc, const double* a, int64_t as,
+                                    const double* f, int64_t fs, double* terms, double* acc,
+                                    double* result, cudaStream_t st) {
+  const long long n = (long long)nxc * nyc;
+  const int K = nyc >= 16 ? 16 : nyc;  // chunks of whole rows
+  static cudaStream_t s2 = nullptr;
+  static cudaEvent_t ev[17];
+  static int dev_of = -1;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess && (s2 == nullptr || dev_of != dev)) {
+    e = cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking);
+    for (int k = 0; e == cudaSuccess && k < 17; ++k)
+      e = cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming);
+    dev_of = dev;
+  }
+  for (int k = 0; e == cudaSuccess && k < K; ++k) {
+    const int r0 = (int)((long long)nyc * k / K), r1 = (int)((long long)nyc * (k + 1) / K);
+    const long long c0 = (long long)r0 * nxc, cn = (long long)(r1 - r0) * nxc;
+    e = launch_w1<1>(M, cn, nxc, a + c0, as, f + 4 * c0, fs, terms + c0, st);
+    if (e == cudaSuccess) e = cudaEventRecord(ev[k], st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s2, ev[k], 0);
+    if (e == cudaSuccess) {
+      k_ordered_sum<<<1, 256, 0, s2>>>(cn, terms + c0, acc, k == 0, n,
+                                       k == K - 1 ? result : nullptr);
+      e = cudaGetLastError();
+    }
+  }
+  if (e == cudaSuccess) e = cudaEventRecord(ev[16], s2);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev[16], 0);
+  return e;
 }
 
 cudaError_t launch_moments(int M, int64_t nq, const double* x, int64_t stride, double* mean,

@@ -53,9 +53,24 @@ def ordered_mean(torch, terms, out=None):
     return out
 
 
+def w1_mean(torch, coarse, fine, out=None, terms=None):
+    """wasserstein1(coarse, restrict(fine)) on the device: per-cell terms and
+    the storage-order mean in one call, the sequential mean overlapped with
+    the terms chunk by chunk (bit-identical to w1_cell_terms + ordered_mean)."""
+    M, nyc, nxc = _check_pair(coarse, fine)
+    if terms is None:
+        terms = torch.empty(nyc * nxc, dtype=torch.float64, device=coarse.device)
+    if out is None:
+        out = torch.empty(2, dtype=torch.float64, device=coarse.device)
+    _check(lib().vlbm_d_w1_restrict_mean(M, nxc, nyc, _ptr(coarse), nyc * nxc, _ptr(fine),
+                                         4 * nyc * nxc, _ptr(terms), _ptr(out[1:]), _ptr(out),
+                                         _stream(torch, coarse)))
+    return out[:1]
+
+
 def wasserstein1(torch, coarse, fine) -> float:
     """wasserstein1(coarse, restrict(fine)) over one variable (bit-exact)."""
-    return float(ordered_mean(torch, w1_cell_terms(torch, coarse, fine)).item())
+    return float(w1_mean(torch, coarse, fine).item())
 
 
 def strong_partials(torch, coarse, fine, out=None):

@@ -200,6 +200,7 @@ def lib() -> C.CDLL:
     sig("vlbm_d_ordered_mean", I, [I64, V, V, V])
     sig("vlbm_d_moments_planes", I, [I, I64, V, V, V, V])
     sig("vlbm_d_w1_rows", I, [I, I, I64, I64, V, V, V, V])
+    sig("vlbm_d_w1_restrict_mean", I, [I, I, I, V, I64, V, I64, V, V, V, V])
     sig("vlbm_ipc_handle", I, [V, C.POINTER(C.c_ubyte), C.POINTER(U64)])
     sig("vlbm_ipc_open", I, [C.POINTER(C.c_ubyte), C.POINTER(V)])
     sig("vlbm_ipc_close", I, [V])
