@@ -16,7 +16,7 @@ for k in k_theta_tiled k_theta_hard k_bisect_cert k_bisect_unc k_bisect_tail k_a
       --nvtx-include timed/ -c 1 -o gpurun_out/r1_$k -f $B --t-start 0.0005 \
       > gpurun_out/r1_ncu_$k.log 2>&1
 done
-for k in ${POST_KERNELS-k_w1_tile k_ordered_mean k_strong_partials}; do
+for k in ${POST_KERNELS-k_w1_tile k_ordered_sum k_strong_partials}; do
   ncu --set full --import-source on --clock-control none -k regex:"$k" -s 1 -c 1 \
       -o gpurun_out/r1_$k -f python tools/post_probe.py 1000 > gpurun_out/r1_ncu_$k.log 2>&1
 done

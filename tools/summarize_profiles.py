@@ -25,7 +25,7 @@ SRC = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "gpurun_out")
 OUT = os.path.join(ROOT, "profiles")
 KERNELS = ["k_theta_tiled", "k_theta_hard", "k_bisect_cert", "k_bisect_unc", "k_bisect_tail",
            "k_advance_tiled",
-           "k_sched", "k_w1_tile", "k_ordered_mean", "k_strong_partials"]
+           "k_sched", "k_w1_tile", "k_ordered_sum", "k_strong_partials"]
 # units of work per launch for the per-item columns: cells of the C2 batch
 # (64 x 1000 x 200) for the march tile kernels, coarse cells (2000 x 400)
 # for the W1 / L1 kernels of configs[3]; the hard-path kernels get None.
