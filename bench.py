@@ -306,17 +306,30 @@ def postproc_bench_dist(torch, dist, dev, ws, rank, M=1000, nxc=2000, nyc=400, r
                      "identical": (w1p == w1) if rank == 0 else None}}
 
 
+METRIC = "VLBM sample-cell updates/s (GLUPS) & % HBM roofline; W1 post-proc cells/s"
+
+
+def workload_config(args, M, ws):
+    """The config object of both arms (same workload, metric and unit)."""
+    return {"workload": f"{'C2 ' if (NX, NY) == (1000, 200) else ''}jet {NX}x{NY}, "
+                        f"M={M}/GPU, RLMP, fp64, steps "
+                        f"{args.warmup}..{args.warmup + args.steps} of each sample",
+            "nx": NX, "ny": NY, "samples_per_gpu": M, "parallelism": f"samples/{ws}",
+            "l2": f"inputs larger than L2 ({2 * 20 * 8 * M * NX * NY / 1e9:.1f} GB "
+                  "state per GPU)"}
+
+
 def run_reference_arm(args):
     ws, rank, local = dist_env()
     if rank != 0:
         return 0
     cb = cpu_reference(args, ws)
-    line = {"impl": "reference", "metric": "VLBM sample-cell updates/s",
+    line = {"impl": "reference", "metric": METRIC,
             "value": cb["value"], "unit": "sample-cell-updates/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"C2 jet {NX}x{NY}, M={M_PER_GPU}/GPU, RLMP, fp64",
-                       "nx": NX, "ny": NY, "samples_per_gpu": M_PER_GPU},
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (jet IC from splitmix64 seeds, base_seed 42)",
+            "config": workload_config(args, args.samples, args.gpus),
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": "sample-cell-updates/s",
                     "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -481,17 +494,12 @@ def main():
                 fp64.update({"achieved": rate, "peak": FP64_PEAK_TINST, "unit": "Tinst/s",
                              "frac": rate / FP64_PEAK_TINST, "fp64_inst_per_cell": ops})
         line = {
-            "metric": "VLBM sample-cell updates/s (GLUPS) & % HBM roofline; W1 post-proc cells/s",
+            "metric": METRIC,
             "value": value, "unit": "sample-cell-updates/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (jet IC from splitmix64 seeds, base_seed 42)",
-            "config": {"workload": f"{'C2 ' if (NX, NY) == (1000, 200) else ''}jet {NX}x{NY}, "
-                                   f"M={M}/GPU, RLMP, fp64, steps "
-                                   f"{args.warmup}..{args.warmup + args.steps} of each sample",
-                       "nx": NX, "ny": NY, "samples_per_gpu": M, "parallelism": f"samples/{ws}",
-                       "l2": f"inputs larger than L2 ({2 * 20 * 8 * M * NX * NY / 1e9:.1f} GB "
-                             "state per GPU)"},
+            "config": workload_config(args, M, ws),
             "glups": value / 1e9,
             "gpu_launches": launches,
             "roofline": roof,
