@@ -11,6 +11,8 @@ python bench.py > gpurun_out/r1_bench.json 2> gpurun_out/r1_bench.err
 B="python bench.py --steps 40 --warmup 3 --no-cpu-baseline --no-postproc --no-e2e --no-roofline"
 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include timed/ -c 600 \
     --csv --log-file gpurun_out/r1_launches.csv $B > gpurun_out/r1_launches.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include timed/ -c 600 \
+    --csv --log-file gpurun_out/r1_launches_late.csv $B --t-start 0.002 > gpurun_out/r1_launches_late.log 2>&1
 for k in k_theta_tiled k_theta_hard k_bisect_cert k_bisect_unc k_bisect_tail k_advance_tiled k_sched; do
   VLBM_GROUPS=1 ncu --set full --import-source on --clock-control none -k regex:"$k" --nvtx \
       --nvtx-include timed/ -c 1 -o gpurun_out/r1_$k -f $B --t-start 0.0005 \

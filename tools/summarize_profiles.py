@@ -82,13 +82,13 @@ def summarize_kernel(k):
     }
 
 
-def launch_share():
-    path = os.path.join(SRC, f"{TAG}_launches.csv")
+def launch_share(suffix=""):
+    path = os.path.join(SRC, f"{TAG}_launches{suffix}.csv")
     if not os.path.exists(path):
         return None
     lines = open(path).read().splitlines()
     start = next(i for i, l in enumerate(lines) if l.startswith('"ID"'))
-    with open(os.path.join(OUT, f"{TAG}_launches.csv"), "w") as f:
+    with open(os.path.join(OUT, f"{TAG}_launches{suffix}.csv"), "w") as f:
         f.write("\n".join(lines[start:]) + "\n")
     rows = list(csv.reader(lines[start:]))
     h = rows[0]
@@ -102,7 +102,7 @@ def launch_share():
     out = [{"kernel": k, "launches": cnt[k], "total_ms": round(tot[k], 3),
             "avg_ms": round(tot[k] / cnt[k], 4), "share_pct": round(100 * tot[k] / all_ms, 1)}
            for k in sorted(tot, key=lambda k: -tot[k])]
-    with open(os.path.join(OUT, f"{TAG}_launch_share.csv"), "w", newline="") as f:
+    with open(os.path.join(OUT, f"{TAG}_launch_share{suffix}.csv"), "w", newline="") as f:
         w = csv.DictWriter(f, fieldnames=list(out[0]))
         w.writeheader()
         w.writerows(out)
@@ -118,6 +118,7 @@ def main():
             w.writeheader()
             w.writerows(rows)
     share = launch_share()
+    late = launch_share("_late")
     by = {r["kernel"]: r for r in rows}
     if "k_theta_tiled" in by and "k_advance_tiled" in by:
         tt, adv = by["k_theta_tiled"], by["k_advance_tiled"]
@@ -132,7 +133,7 @@ def main():
             json.dump(fp, f, indent=1)
     for r in rows:
         print(r)
-    for r in share or []:
+    for r in (share or []) + (late or []):
         print(r)
 
 
