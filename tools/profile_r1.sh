@@ -8,7 +8,7 @@
 # tools/summarize_profiles.py turns these into profiles/r1_*.
 mkdir -p gpurun_out
 python bench.py > gpurun_out/r1_bench.json 2> gpurun_out/r1_bench.err
-B="python bench.py --steps 40 --warmup 3 --no-cpu-baseline --no-postproc --no-e2e --no-roofline"
+B="python bench.py --steps 40 --warmup 3 --no-cpu-baseline --no-postproc --no-e2e --no-roofline --no-late"
 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include timed/ -c 600 \
     --csv --log-file gpurun_out/r1_launches.csv $B > gpurun_out/r1_launches.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include timed/ -c 600 \
