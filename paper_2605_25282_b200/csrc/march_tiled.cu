@@ -646,10 +646,14 @@ __device__ __forceinline__ void load_unc_entry(const MarchParams& P, int s, long
   h.unc = kAllVertices & ~((h.lo_all ? kAllVertices : 0u) & h.mhi);
 }
 
-// Steps a replayed bisection may evaluate exactly in k_bisect_unc; a cell
+// Steps a replayed bisection may evaluate exactly in k_bisect_unc (1 measured
+// best of 0, 1, 2, 4, 6); a cell
 // that needs more (its classifications leave a wide band) continues in
 // k_bisect_tail, so no warp waits on one lane's long exact tail.
-constexpr int kReplayInline = 2;
+#ifndef VLBM_REPLAY_INLINE
+#define VLBM_REPLAY_INLINE 1
+#endif
+constexpr int kReplayInline = VLBM_REPLAY_INLINE;
 
 // blockIdx.y = cq bin; bins run concurrently.
 #ifndef VLBM_UNC_MINB

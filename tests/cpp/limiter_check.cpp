@@ -95,7 +95,7 @@ int main(int argc, char** argv) {
     bad_queued += !same(q, want);
     Bracket br;
     double t;
-    if (bisect_replay(fo, cf, delta, b, h, gm1, 2, br, audit)) {
+    if (bisect_replay(fo, cf, delta, b, h, gm1, 1, br, audit)) {
       t = br.lo;
     } else {
       ++stopped;
