@@ -59,6 +59,26 @@ def test_config1_bitwise_per_step(vlbm, vo):
         assert_bitwise(sim.theta_cell(m), r.theta_cell(), f"theta sample {m}")
 
 
+@pytest.mark.parametrize("nx,ny", [(4, 4), (37, 11), (33, 17), (66, 9), (97, 23)])
+def test_ragged_grids_bitwise(vlbm, vo, nx, ny):
+    """Grids that are not multiples of the 32x8 tiles (partial tiles, tiles
+    touching several boundaries, the minimum 4x4 grid): the jet with square
+    cells (x_max = 0.5 nx / ny), 30 steps, u, pops and cell theta
+    bit-identical to the oracle."""
+    x_max = 0.5 * nx / ny
+    g = vlbm.Grid(nx, ny, x_max)
+    sim = vlbm.BatchSimulation.jet(g, n_samples=2, base_seed=7)
+    sim.step(30)
+    for m in range(2):
+        r = vo.jet_sim(make_grid(nx, ny, x_max), make_params(), make_pert(), 7, m)
+        for _ in range(30):
+            r.step(r.suggest_dt())
+        u, p = r.get(pops=True)
+        assert_bitwise(sim.state(m), u, f"u {nx}x{ny} sample {m}")
+        assert_bitwise(sim.populations(m), p, f"pops {nx}x{ny} sample {m}")
+        assert_bitwise(sim.theta_cell(m), r.theta_cell(), f"theta {nx}x{ny} sample {m}")
+
+
 def test_run_samples_matches_run_sample(vlbm, vo):
     """run_samples == run_sample for every snapshot of 3 samples on the smoke
     grid 125x25 to t_end = 0.003 (times, diverged flags, steps, fields)."""
