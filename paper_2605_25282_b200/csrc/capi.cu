@@ -231,6 +231,8 @@ int alloc_batch(const vlbm_grid* g, const vlbm_params* p, int S, int device, vlb
       size_t cap = (size_t)Q.S * P.nx * P.ny;
       if (cap * entry > avail / 2 / G) cap = avail / 2 / G / entry;
       if (cap > (size_t)INT_MAX / 2) cap = (size_t)INT_MAX / 2;
+      if (const char* e = getenv("VLBM_HQ_CAP"))  // test hook: exercise the overflow paths
+        cap = std::min(cap, (size_t)std::max(0ll, atoll(e)));
       cap = cap / 768 * 768;  // even thirds of whole kHB chunks: 16-B aligned bulk copies
       if (cap >= 1024) {
         Q.hq_cap = (int)cap;

@@ -310,3 +310,23 @@ def test_certified_bisection_audit_and_late_time_parity(vlbm, vo):
             r.step(min(r.suggest_dt(), 0.0009 - r.time))
         assert steps[m] == r.steps
         assert_bitwise(sim.state(m), r.get(), f"late-time sample {m}")
+
+
+@pytest.mark.parametrize("cap", ["1536", "0"])
+def test_limiter_queue_overflow_paths_bitwise(vlbm, vo, monkeypatch, cap):
+    """A limiter queue far smaller than the hard cells (VLBM_HQ_CAP test hook):
+    CTAs whose cells do not fit finish them in place (tile pass, stage,
+    bisection tail) -- and with no queue at all (cap 0) every hard cell is
+    finished by its tile thread.  Fields bit-identical to the oracle at late
+    time."""
+    monkeypatch.setenv("VLBM_HQ_CAP", cap)
+    g = vlbm.Grid(200, 40)
+    sim = vlbm.BatchSimulation.jet(g, n_samples=4, base_seed=42)
+    sim.run_to(0.0008)
+    t, steps, status = sim.scalars()
+    for m in (0, 3):
+        r = vo.jet_sim(make_grid(200, 40), make_params(), make_pert(), 42, m)
+        while r.time < 0.0008 - 1e-12:
+            r.step(min(r.suggest_dt(), 0.0008 - r.time))
+        assert steps[m] == r.steps
+        assert_bitwise(sim.state(m), r.get(), f"overflow cap {cap} sample {m}")
