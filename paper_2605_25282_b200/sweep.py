@@ -96,15 +96,31 @@ def grid_sweep(torch, nx0: int, ny0: int, levels: int, n_samples: int,
                lattice: LatticeParams = LatticeParams(), gas: GasParams = GasParams(),
                pp: PerturbationParams = PerturbationParams(), strip_width: float = 0.02,
                metric_variable: int = 0, require_positivity: bool = False, m0: int = 0,
-               batch: Optional[int] = None, device: int = 0) -> SweepReport:
+               batch: Optional[int] = None, device: int = 0, dist=None,
+               group=None) -> Optional[SweepReport]:
     """Grids nx0 x ny0 * 2^l (l = 0..levels-1), M = n_samples samples each,
     snapshots at ``times``; returns the rows and rates compute_metrics would
-    write (metrics.csv / rates.csv)."""
+    write (metrics.csv / rates.csv).
+
+    With ``dist`` (torch.distributed, one process per GPU) the samples are
+    sharded: rank r marches its contiguous share on every level
+    with no communication; per pair and time the joint validity masks are
+    gathered, W1 runs as dist.peer_wasserstein1 (each rank's kernel reads the
+    other ranks' snapshots through CUDA-IPC peer mappings, no re-shard) and
+    E_strong from the ranks' per-sample partials gathered in sample order.
+    Rank 0 returns the report (bit-identical to one process); the other ranks
+    return None."""
     if levels < 2:
         raise RuntimeError("metrics: need >= 2 grids for Cauchy errors")
     times = list(times)
-    M = n_samples
-    batch = batch or M
+    M_total = n_samples
+    if dist is not None:
+        from .dist import shard_range
+        s0, M = shard_range(M_total, dist.get_world_size(group), dist.get_rank(group))
+        m0 += s0
+    else:
+        M = M_total
+    batch = batch or max(M, 1)
     dev = torch.device("cuda", device)
     grids = [Grid(nx0 << l, ny0 << l) for l in range(levels)]
     store, valid = [], []  # store[l][ti]: (M, 4, ny, nx) device tensor; valid[l]: bool (M,)
@@ -133,6 +149,9 @@ def grid_sweep(torch, nx0: int, ny0: int, levels: int, n_samples: int,
     n_pairs = levels - 1
     w1s = [[0.0] * len(times) for _ in range(n_pairs)]
     strongs = [[0.0] * len(times) for _ in range(n_pairs)]
+    if dist is not None:
+        return _sharded_metrics(torch, dist, group, grids, times, store, valid, metric_variable,
+                                rep, w1s, strongs)
     for p in range(n_pairs):
         cg, fg = grids[p], grids[p + 1]
         mask = valid[p] & valid[p + 1]
@@ -154,6 +173,11 @@ def grid_sweep(torch, nx0: int, ny0: int, levels: int, n_samples: int,
             es = post.strong_finish(part.cpu().numpy())
             rep.rows.append(MetricsRow(float(t), f"{cg.nx}->{fg.nx}", m_star, w1, es))
             w1s[p][ti], strongs[p][ti] = w1, es
+    return _finish_rates(rep, grids, times, w1s, strongs)
+
+
+def _finish_rates(rep, grids, times, w1s, strongs):
+    n_pairs = len(grids) - 1
     dxs = [g.dx() for g in grids[:-1]]
 
     def safe_fit(e):
@@ -166,3 +190,45 @@ def grid_sweep(torch, nx0: int, ny0: int, levels: int, n_samples: int,
         rep.rates.append(RateRow(float(t), safe_fit([w1s[p][ti] for p in range(n_pairs)]),
                                  safe_fit([strongs[p][ti] for p in range(n_pairs)])))
     return rep
+
+
+def _sharded_metrics(torch, dist, group, grids, times, store, valid, k, rep, w1s, strongs):
+    """The metrics of a sample-sharded sweep (see grid_sweep)."""
+    from .dist import distributed_strong_error, peer_wasserstein1
+    rank = dist.get_rank(group)
+    host = dist.get_backend(group) == "gloo"
+    for label in list(rep.steps):  # per-sample step counts of every rank, in sample order
+        parts = [None] * dist.get_world_size(group)
+        dist.all_gather_object(parts, rep.steps[label].tolist(), group=group)
+        rep.steps[label] = np.array([x for q in parts for x in q], np.int64)
+    for p in range(len(grids) - 1):
+        cg, fg = grids[p], grids[p + 1]
+        mask = valid[p] & valid[p + 1]
+        counts = [None] * dist.get_world_size(group)
+        dist.all_gather_object(counts, int(mask.sum()), group=group)
+        m_star = sum(counts)
+        if m_star < 1:
+            raise RuntimeError("metrics: no jointly valid samples for pair")
+        dev = store[p][0].device
+        keep = torch.from_numpy(np.flatnonzero(mask)).to(dev)
+        vmask = torch.from_numpy(mask)
+        for ti, t in enumerate(times):
+            c = store[p][ti]
+            f = store[p + 1][ti]
+            M = c.shape[0]
+            w1 = peer_wasserstein1(torch, dist, c[:, k].reshape(M, -1).contiguous(),
+                                   f[:, k].reshape(M, -1).contiguous(), vmask, cg.nx, group)
+            cv = c.index_select(0, keep).contiguous()
+            fv = f.index_select(0, keep).contiguous()
+            part = torch.empty((cv.shape[0], 10), dtype=torch.float64, device=dev)
+            if cv.shape[0]:
+                _check(lib().vlbm_d_strong_partials(cv.shape[0], cg.nx, cg.ny, cv.data_ptr(),
+                                                    fv.data_ptr(), part.data_ptr(),
+                                                    torch.cuda.current_stream(dev).cuda_stream))
+            es = distributed_strong_error(torch, dist, part.cpu() if host else part, group)
+            if rank == 0:
+                rep.rows.append(MetricsRow(float(t), f"{cg.nx}->{fg.nx}", m_star, w1, es))
+                w1s[p][ti], strongs[p][ti] = w1, es
+    if rank != 0:
+        return None
+    return _finish_rates(rep, grids, times, w1s, strongs)

@@ -61,3 +61,47 @@ def test_fit_rate_restatement_bitwise(ref, n):
         dx = sorted(rng.uniform(1e-4, 1e-1, size=n), reverse=True)
         assert bits(sweep.fit_rate(e, dx)) == bits(ref.fit_rate(e, dx))
 
+
+
+def _sweep_worker(rank, world, port, q):
+    import os
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2605_25282_b200 import sweep
+    rep = sweep.grid_sweep(torch, 40, 8, 3, 5, [0.0, 2e-4, 4e-4], base_seed=11, dist=dist)
+    if rank == 0:
+        q.put([(r.pair, r.time, r.m_star, float(r.w1).hex(), float(r.e_strong).hex())
+               for r in rep.rows] + [(float(r.r_w1).hex(), float(r.r_strong).hex())
+                                     for r in rep.rates] + [rep.steps["160x32"].tolist()])
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_grid_sweep_sharded_equals_single_process():
+    """grid_sweep with the samples sharded over 2 processes (sharing the one
+    GPU: real CUDA-IPC peer mappings, gloo for the host exchange) gives rank 0
+    the single-process report bit for bit."""
+    import socket
+    import torch.multiprocessing as mp
+    from paper_2605_25282_b200 import sweep
+    rep = sweep.grid_sweep(torch, 40, 8, 3, 5, [0.0, 2e-4, 4e-4], base_seed=11)
+    want = [(r.pair, r.time, r.m_star, float(r.w1).hex(), float(r.e_strong).hex())
+            for r in rep.rows] + [(float(r.r_w1).hex(), float(r.r_strong).hex())
+                                  for r in rep.rates] + [rep.steps["160x32"].tolist()]
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_sweep_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert got == want
