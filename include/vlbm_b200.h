@@ -122,6 +122,8 @@ typedef struct vlbm_batch vlbm_batch;
 
 /* ---- library ---------------------------------------------------------- */
 int vlbm_abi_version(void);
+/* Visible CUDA devices (0 without a GPU). */
+int vlbm_device_count(void);
 const char* vlbm_last_error(void);
 /* Fills the reference defaults (lattice.hpp:13-35, euler.hpp:10,
  * perturbation.hpp:16-31, config.hpp:27-29) and the jet boundaries. */

@@ -19,7 +19,11 @@
 #pragma once
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <exception>
+#include <mutex>
+#include <thread>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -145,11 +149,95 @@ inline std::vector<SampleResult> run_samples(const std::vector<SampleSpec>& spec
   return out;
 }
 
+// The batches of one grid of run_ensemble spread over `ndev` GPUs (see
+// run_ensemble).  Returns false when should_stop ended the run early.
+inline bool run_grid_on_devices(const CaseConfig& cfg, EnsembleManifest& man, std::size_t gi,
+                                const std::vector<int>& todo, int ndev, int batch_samples,
+                                const std::filesystem::path& manifest_path, EnsembleProgress& prog,
+                                const std::function<void(const EnsembleProgress&)>& progress,
+                                const std::function<bool()>& should_stop) {
+  const Grid grid = cfg.make_grid(gi);
+  const std::string grid_dir = "grid_" + grid.label();
+  const std::filesystem::path root = cfg.output_dir;
+  std::vector<std::pair<std::size_t, std::size_t>> batches;
+  // enough batches to keep every device busy, at most batch_samples each
+  const std::size_t per = std::max<std::size_t>(
+      1, std::min<std::size_t>(batch_samples, (todo.size() + ndev - 1) / ndev));
+  for (std::size_t b0 = 0; b0 < todo.size(); b0 += per)
+    batches.emplace_back(b0, std::min(todo.size(), b0 + per));
+  std::mutex mu;
+  std::size_t next = 0;
+  bool stopped = false;
+  std::exception_ptr err;
+  auto worker = [&](int dev) {
+    for (;;) {
+      std::size_t k;
+      {
+        std::lock_guard<std::mutex> lock(mu);
+        if (stopped || err || next >= batches.size()) return;
+        if (should_stop && should_stop()) {
+          stopped = true;
+          return;
+        }
+        k = next++;
+      }
+      try {
+        const auto [b0, b1] = batches[k];
+        std::vector<SampleSpec> specs;
+        for (std::size_t q = b0; q < b1; ++q) {
+          SampleSpec spec;
+          spec.grid = grid;
+          spec.lattice = cfg.lattice;
+          spec.gas = cfg.gas;
+          spec.perturbation = cfg.perturbation;
+          spec.coeffs = man.samples[todo[q]].coeffs;
+          spec.inlet_strip_width = cfg.inlet_strip_width;
+          spec.snapshot_times = cfg.snapshot_times;
+          specs.push_back(std::move(spec));
+        }
+        const std::vector<SampleResult> results =
+            run_samples(specs, dev % std::max(1, vlbm_device_count()));
+        std::lock_guard<std::mutex> lock(mu);
+        for (std::size_t q = b0; q < b1; ++q) {
+          const int m = todo[q];
+          const SampleResult& res = results[q - b0];
+          std::vector<std::string> rel_files;
+          for (std::size_t ti = 0; ti < res.snapshots.size(); ++ti) {
+            const std::string rel = grid_dir + "/" + snapshot_filename(m, static_cast<int>(ti));
+            write_snapshot(res.snapshots[ti], root / rel);
+            rel_files.push_back(rel);
+          }
+          const bool ok = res.admissible &&
+                          admissibility_flag(res.snapshots, cfg.gas, cfg.positivity_admissibility);
+          man.samples[m].status[gi] = ok ? RunStatus::Admissible : RunStatus::Diverged;
+          man.samples[m].files[gi] = rel_files;
+          write_manifest(man, manifest_path);
+          ++prog.completed;
+          if (!ok) ++prog.diverged;
+          if (progress) progress(prog);
+        }
+      } catch (...) {
+        std::lock_guard<std::mutex> lock(mu);
+        if (!err) err = std::current_exception();
+        return;
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int d = 0; d < ndev; ++d) pool.emplace_back(worker, d);
+  for (auto& t : pool) t.join();
+  if (err) std::rethrow_exception(err);
+  return !stopped;
+}
+
 // run_ensemble (ensemble.hpp:235-342) with the march on the GPU.  Same
 // manifest (format, atomic rewrite after every completion, byte-identical
 // config check on resume), same snapshot files and statuses; the work unit is
 // a batch of up to `batch_samples` NotRun samples of one grid instead of one
 // (sample, grid) task per CPU thread.  should_stop is polled between batches.
+// device < 0: every visible GPU, one host thread per device taking batches
+// from a shared list (the reference's worker pool with GPUs as workers; the
+// snapshot writes and manifest updates are serialised by a mutex, as there).
 inline EnsembleManifest run_ensemble(
     const CaseConfig& cfg, const std::function<void(const EnsembleProgress&)>& progress = {},
     const std::function<bool()>& should_stop = {}, int device = 0, int batch_samples = 1024) {
@@ -192,6 +280,19 @@ inline EnsembleManifest run_ensemble(
     std::vector<int> todo;
     for (int m = 0; m < cfg.samples; ++m)
       if (man.samples[m].status[gi] == RunStatus::NotRun) todo.push_back(m);
+    // workers: every visible GPU (VLBM_DEVICES overrides the count; worker w
+    // runs on device w mod the visible count -- a test hook for this path)
+    int ndev = 1;
+    if (device < 0) {
+      ndev = std::max(1, vlbm_device_count());
+      if (const char* e = std::getenv("VLBM_DEVICES")) ndev = std::max(1, std::atoi(e));
+    }
+    if (ndev > 1) {
+      if (!run_grid_on_devices(cfg, man, gi, todo, ndev, batch_samples, manifest_path, prog,
+                               progress, should_stop))
+        return man;
+      continue;
+    }
     for (std::size_t b0 = 0; b0 < todo.size(); b0 += batch_samples) {
       if (should_stop && should_stop()) return man;
       const std::size_t b1 = std::min(todo.size(), b0 + static_cast<std::size_t>(batch_samples));
@@ -207,7 +308,7 @@ inline EnsembleManifest run_ensemble(
         spec.snapshot_times = cfg.snapshot_times;
         specs.push_back(std::move(spec));
       }
-      const std::vector<SampleResult> results = run_samples(specs, device);
+      const std::vector<SampleResult> results = run_samples(specs, device < 0 ? 0 : device);
       for (std::size_t q = b0; q < b1; ++q) {
         const int m = todo[q];
         const SampleResult& res = results[q - b0];

@@ -390,6 +390,10 @@ int read_ctl(vlbm_batch* b, std::vector<SampleCtl>& ctl) {
 extern "C" {
 
 int vlbm_abi_version(void) { return VLBM_ABI_VERSION; }
+int vlbm_device_count(void) {
+  int n = 0;
+  return cudaGetDeviceCount(&n) == cudaSuccess ? n : 0;
+}
 const char* vlbm_last_error(void) { return vlbm_impl::g_last_error.c_str(); }
 
 int vlbm_batch_create(const vlbm_grid* g, const vlbm_params* p, const vlbm_perturbation* pp,

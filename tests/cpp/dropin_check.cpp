@@ -8,6 +8,8 @@
 //   dropin_check ensemble <dir> [M] reference run_ensemble vs gpu::run_ensemble
 //                                   on a smoke-style case: byte-identical
 //                                   output directories (manifest + snapshots)
+//   dropin_check ensemble_all <dir> [M]  the same through the multi-GPU worker
+//                                   path (run_ensemble device -1; VLBM_DEVICES)
 //   dropin_check metrics <dir>      compute_metrics vs gpu::compute_metrics on
 //                                   that ensemble: identical rows (bitwise)
 //   dropin_check outputs <dir>      metrics / rates CSVs (write_metrics_csv) and
@@ -94,14 +96,14 @@ static int check_nogpu() {
   return 1;
 }
 
-static int check_ensemble(const fs::path& dir, int M) {
+static int check_ensemble(const fs::path& dir, int M, int device = 0) {
   const fs::path run = dir / "run", cpu = dir / "cpu";
   fs::remove_all(dir);
   const CaseConfig cfg = smoke_case(run.string(), M);
   run_ensemble(cfg);  // the reference, on all host threads
   fs::rename(run, cpu);
   int calls = 0;
-  gpu::run_ensemble(cfg, [&calls](const EnsembleProgress&) { ++calls; });
+  gpu::run_ensemble(cfg, [&calls](const EnsembleProgress&) { ++calls; }, {}, device);
   const auto a = dir_bytes(cpu), b = dir_bytes(run);
   int diff = 0;
   for (const auto& [k, v] : a) {
@@ -319,6 +321,8 @@ int main(int argc, char** argv) {
     if (mode == "ic") return check_ic();
     if (mode == "nogpu") return check_nogpu();
     if (mode == "ensemble" && argc >= 3) return check_ensemble(argv[2], argc > 3 ? std::atoi(argv[3]) : 8);
+    if (mode == "ensemble_all" && argc >= 3)  // device -1: the multi-GPU worker path
+      return check_ensemble(argv[2], argc > 3 ? std::atoi(argv[3]) : 8, -1);
     if (mode == "metrics" && argc >= 3) return check_metrics(argv[2]);
     if (mode == "outputs" && argc >= 3) return check_outputs(argv[2]);
     if (mode == "acceptance" && argc >= 3) return check_acceptance(argv[2]);

@@ -94,3 +94,21 @@ def test_reference_acceptance_criteria_6_to_9_on_gpu():
     for num, want in gold["criteria"].items():
         assert got[num]["verdict"] == want["verdict"], (num, got[num], want)
         assert got[num]["detail"] == want["detail"], (num, got[num], want)
+
+
+@pytest.mark.gpu
+def test_gpu_run_ensemble_multi_device_workers_byte_identical():
+    """gpu::run_ensemble(device = -1): one host thread per GPU taking batches
+    from a shared list, snapshot writes and manifest updates under a mutex.
+    This box has one GPU, so VLBM_DEVICES=3 runs three workers on it; the
+    output directory must still equal the reference run_ensemble's bytes."""
+    if not os.path.exists(BIN):
+        pytest.skip("dropin_check not built")
+    d = tempfile.mkdtemp(prefix="vlbm_dropin_mt_")
+    env = dict(os.environ, VLBM_DEVICES="3")
+    try:
+        r = subprocess.run([BIN, "ensemble_all", d, "8"], capture_output=True, text=True,
+                           timeout=900, env=env)
+        assert r.returncode == 0, r.stdout + r.stderr
+    finally:
+        shutil.rmtree(d, ignore_errors=True)
