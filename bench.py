@@ -263,20 +263,7 @@ def postproc_bench_dist(torch, dist, dev, ws, rank, M=1000, nxc=2000, nyc=400, r
                                                  restricted[m].data_ptr(), stream))
         return vd.distributed_wasserstein1(torch, dist, coarse, restricted, valid)
 
-    w1 = once()
-    times = []
-    for _ in range(reps):
-        dist.barrier()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        w1 = once()
-        e1.record()
-        torch.cuda.synchronize()
-        t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=d)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        times.append(float(t.item()))
-    ms = statistics.median(times)
+    host = dist.get_backend() == "gloo"
 
     def timed(fn):
         fn()
@@ -289,21 +276,32 @@ def postproc_bench_dist(torch, dist, dev, ws, rank, M=1000, nxc=2000, nyc=400, r
             r = fn()
             e1.record()
             torch.cuda.synchronize()
-            t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=d)
+            t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64,
+                             device="cpu" if host else d)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ts.append(float(t.item()))
         return r, statistics.median(ts)
 
+    out = {"workload": f"C4 synthetic log-normal rho, M={M} sharded over {ws} ranks, coarse "
+                       f"{nxc}x{nyc} vs restricted fine {2 * nxc}x{2 * nyc}; restriction + "
+                       "2 NCCL all_to_all + per-cell terms + ordered gather + sequential mean",
+           "n_gpus": ws}
+    w1 = None
+    try:
+        w1, ms = timed(once)
+        out.update({"w1_cells_per_s": nc / (ms * 1e-3), "w1_ms": ms, "W1": w1})
+    except Exception as exc:  # e.g. all_to_all on a gloo group of ranks sharing a GPU
+        out["error"] = f"{type(exc).__name__}: {exc}"
     # the fused alternative: no re-shard, each rank's kernel reads the other
     # ranks' planes through CUDA-IPC peer mappings (NVLink) while it sorts
-    w1p, msp = timed(lambda: vd.peer_wasserstein1(torch, dist, coarse, fine, valid, nxc))
-    return {"workload": f"C4 synthetic log-normal rho, M={M} sharded over {ws} ranks, coarse "
-                        f"{nxc}x{nyc} vs restricted fine {2 * nxc}x{2 * nyc}; restriction + "
-                        "2 NCCL all_to_all + per-cell terms + ordered gather + sequential mean",
-            "w1_cells_per_s": nc / (ms * 1e-3), "w1_ms": ms, "W1": w1, "n_gpus": ws,
-            "peer": {"how": "vlbm_d_w1_rows over CUDA-IPC peer mappings (no all_to_all)",
-                     "w1_cells_per_s": nc / (msp * 1e-3), "w1_ms": msp, "W1": w1p,
-                     "identical": (w1p == w1) if rank == 0 else None}}
+    try:
+        w1p, msp = timed(lambda: vd.peer_wasserstein1(torch, dist, coarse, fine, valid, nxc))
+        out["peer"] = {"how": "vlbm_d_w1_rows over CUDA-IPC peer mappings (no all_to_all)",
+                       "w1_cells_per_s": nc / (msp * 1e-3), "w1_ms": msp, "W1": w1p,
+                       "identical": (w1p == w1) if rank == 0 and w1 is not None else None}
+    except Exception as exc:
+        out["peer"] = {"error": f"{type(exc).__name__}: {exc}"}
+    return out
 
 
 METRIC = "VLBM sample-cell updates/s (GLUPS) & % HBM roofline; W1 post-proc cells/s"
@@ -371,10 +369,17 @@ def main():
     import torch
 
     ws, rank, local = dist_env()
+    # one GPU per rank; on a box with fewer GPUs than ranks (a test of the
+    # multi-rank path only) ranks share them round-robin
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("VLBM_BENCH_BACKEND", "nccl")  # gloo: ranks sharing a GPU
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     import paper_2605_25282_b200 as v
 
     M = args.samples
@@ -385,6 +390,18 @@ def main():
         if ws > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
+
+    def _reduce(x, op):  # device tensors on NCCL, host tensors on gloo
+        dv = "cpu" if torch.distributed.get_backend() == "gloo" else "cuda"
+        t = torch.tensor([float(x)], device=dv, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=op)
+        return float(t.item())
+
+    def reduce_max(x):
+        return _reduce(x, torch.distributed.ReduceOp.MAX)
+
+    def reduce_sum(x):
+        return _reduce(x, torch.distributed.ReduceOp.SUM)
 
     # ---- device-resident march ----
     sim = v.BatchSimulation.jet(g, lat, gas, pp, base_seed=42, m0=rank * M, n_samples=M,
@@ -416,12 +433,8 @@ def main():
     t_max = ms
     upd_total = updates
     if ws > 1:
-        tt = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        t_max = float(tt.item())
-        uu = torch.tensor([updates], device="cuda", dtype=torch.float64)
-        torch.distributed.all_reduce(uu)
-        upd_total = float(uu.item())
+        t_max = reduce_max(ms)
+        upd_total = reduce_sum(updates)
     value = upd_total / (t_max * 1e-3)
     sim.close()
 
@@ -444,9 +457,7 @@ def main():
         e.close()
         et = t1 - t0
         if ws > 1:
-            tt = torch.tensor([et], device="cuda", dtype=torch.float64)
-            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-            et = float(tt.item())
+            et = reduce_max(et)
         h2d = M * (4 * NX * NY + 4 * NY) * 8
         e2e = {"value": st["cell_updates"] * ws / et, "unit": "sample-cell-updates/s",
                "h2d_bytes_per_step": int(h2d / args.steps),
@@ -476,11 +487,7 @@ def main():
         lms = e0.elapsed_time(e1)
         lupd = l1["cell_updates"] - l0["cell_updates"]
         if ws > 1:
-            tt = torch.tensor([lms, float(lupd)], device="cuda", dtype=torch.float64)
-            mx = tt[:1].clone()
-            torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
-            torch.distributed.all_reduce(tt[1:])
-            lms, lupd = float(mx.item()), float(tt[1].item())
+            lms, lupd = reduce_max(lms), reduce_sum(lupd)
         t_end = float(lt.scalars()[0].min())
         lt.close()
         late = {"value": lupd / (lms * 1e-3), "unit": "sample-cell-updates/s",
