@@ -739,17 +739,26 @@ cudaError_t launch_w1_restrict_mean(int M, int nxc, int nyc, const double* a, in
                                     double* result, cudaStream_t st) {
   const long long n = (long long)nxc * nyc;
   const int K = nyc >= 16 ? 16 : nyc;  // chunks of whole rows
-  static cudaStream_t s2 = nullptr;
-  static cudaEvent_t ev[17];
-  static int dev_of = -1;
+  // the second stream and its events: one set per host thread and device
+  // (concurrent callers on several GPUs each get their own)
+  struct Aux {
+    int dev = -1;
+    cudaStream_t s2 = nullptr;
+    cudaEvent_t ev[17] = {};
+  };
+  thread_local Aux aux[16];
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
-  if (e == cudaSuccess && (s2 == nullptr || dev_of != dev)) {
-    e = cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking);
+  if (e == cudaSuccess && (dev < 0 || dev >= 16)) e = cudaErrorInvalidDevice;
+  Aux* ax = e == cudaSuccess ? &aux[dev] : nullptr;
+  if (e == cudaSuccess && ax->dev != dev) {
+    e = cudaStreamCreateWithFlags(&ax->s2, cudaStreamNonBlocking);
     for (int k = 0; e == cudaSuccess && k < 17; ++k)
-      e = cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming);
-    dev_of = dev;
+      e = cudaEventCreateWithFlags(&ax->ev[k], cudaEventDisableTiming);
+    if (e == cudaSuccess) ax->dev = dev;
   }
+  cudaStream_t s2 = ax ? ax->s2 : nullptr;
+  cudaEvent_t* ev = ax ? ax->ev : nullptr;
   for (int k = 0; e == cudaSuccess && k < K; ++k) {
     const int r0 = (int)((long long)nyc * k / K), r1 = (int)((long long)nyc * (k + 1) / K);
     const long long c0 = (long long)r0 * nxc, cn = (long long)(r1 - r0) * nxc;
