@@ -23,6 +23,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <mutex>
+
 #include "internal.h"
 #include "march.cuh"
 #include "march_common.cuh"
@@ -833,8 +835,17 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_ADV_MINB)
 namespace vlbm_impl {
 using namespace vlbm_dev;
 
+// The dynamic shared-memory opt-ins are per device (each device's context
+// holds its own copy of the kernels): set once per device.
 static cudaError_t smem_attrs() {
-  static const cudaError_t done = [] {
+  static std::mutex mu;
+  static int done_mask[4] = {0, 0, 0, 0};  // bit per device id < 128
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev)) return e;
+  if (dev < 0 || dev >= 128) return cudaErrorInvalidDevice;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done_mask[dev >> 5] >> (dev & 31) & 1) return cudaSuccess;
+  const cudaError_t r = [] {
     cudaError_t e = cudaFuncSetAttribute(k_theta_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)tiled::kThetaSmem);
     if (e == cudaSuccess)
@@ -851,7 +862,8 @@ static cudaError_t smem_attrs() {
                                (int)tiled::kAdvanceSmem);
     return e;
   }();
-  return done;
+  if (r == cudaSuccess) done_mask[dev >> 5] |= 1 << (dev & 31);
+  return r;
 }
 
 static_assert(tiled::TX == 32 && tiled::TY == 8 && tiled::NT == 256, "theta_tiles() layout");
