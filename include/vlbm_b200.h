@@ -27,6 +27,16 @@
  *   vlbm_strong_error        strong_error                   metrics.hpp:55-90
  *   vlbm_wasserstein1        wasserstein1                   metrics.hpp:97-125
  *   vlbm_ensemble_moments    ensemble_moments               metrics.hpp:148-177
+ *   vlbm_d_w1_restrict_mean  wasserstein1 on device planes  metrics.hpp:97-125
+ *                            (restriction fused, storage-order mean overlapped)
+ *   vlbm_d_w1_rows           wasserstein1's per-cell terms over samples held on
+ *                            several GPUs (row tables, CUDA-IPC peer mappings):
+ *                            compute_metrics' W1 across a sample-sharded node
+ *   vlbm_batch_copy_fields_device
+ *                            the snapshots of run_sample kept on the device
+ *                            (compute_metrics without the .vlbm round trip)
+ *   vlbm_device_count        run_ensemble's worker count    ensemble.hpp:294-300
+ *                            (one worker per GPU)
  *
  * Layouts.  A "field" is the reference FieldSnapshot data in the .vlbm
  * on-disk plane order (snapshot_io.hpp:311-315): 4 contiguous f64 planes
