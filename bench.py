@@ -563,7 +563,7 @@ def main():
             line["late_window"] = late
         if post:
             line["postproc"] = post
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and ws == 1:  # the reference CPU path: N = 1 only
             line["cpu_baseline"] = cpu_reference(args, ws)
         print(json.dumps(line), flush=True)
     if ws > 1:
