@@ -15,6 +15,8 @@
 #include <cstdlib>
 #include <cstring>
 using std::isfinite;
+using std::isinf;
+using std::isnan;
 #define __device__
 #define __host__
 #define __forceinline__ inline
@@ -104,12 +106,32 @@ int main(int argc, char** argv) {
     bad_replay += !same(t, want);
   }
   std::fclose(f);
+  // hypot_ref (signal speed with the conservative bound) against this host's
+  // libm hypot over the whole double range, deterministic pseudo-random pairs
+  long hyp_n = 0, hyp_bad = 0;
+  unsigned long long st = 0x9e3779b97f4a7c15ull;
+  auto next = [&st] {
+    unsigned long long z = (st += 0x9e3779b97f4a7c15ull);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+  };
+  for (int q = 0; q < 400000; ++q) {
+    const double a = (double)(next() >> 11) * 0x1p-53, bb = (double)(next() >> 11) * 0x1p-53;
+    const int e1 = (int)(next() % 2000) - 1000, e2 = e1 + (int)(next() % 200) - 100;
+    double x = std::ldexp(a, e1), y = std::ldexp(bb, e2 < -1074 ? -1074 : (e2 > 1000 ? 1000 : e2));
+    if (next() & 1) x = -x;
+    if (q % 3 == 0) x = a * 4000.0, y = bb * 4000.0;  // the jet's momentum range
+    const double want = std::hypot(x, y), got = hypot_ref(x, y);
+    ++hyp_n;
+    hyp_bad += !same(want, got);
+  }
   std::printf(
       "{\"cells\": %ld, \"theta_one\": %ld, \"certified_at_one\": %ld, \"certificate_errors\": %ld, "
       "\"hard\": %ld, \"bisections\": %ld, \"replay_stopped\": %ld, \"mismatch_plain\": %ld, "
       "\"mismatch_queued\": %ld, \"mismatch_replay\": %ld, \"audit_errors\": %d, "
-      "\"margin_errors\": %ld}\n",
+      "\"margin_errors\": %ld, \"hypot_checks\": %ld, \"hypot_errors\": %ld}\n",
       cells, at_one, cert, cert_bad, hard, bisect, stopped, bad_plain, bad_queued, bad_replay,
-      audit[0], margin_bad);
+      audit[0], margin_bad, hyp_n, hyp_bad);
   return 0;
 }

@@ -361,3 +361,27 @@ def test_sod_tube_bitwise(vlbm, vo, limiter):
     assert_bitwise(sim.state(0), u, "sod u")
     assert_bitwise(sim.populations(0), pops, "sod pops")
     assert sim.state(0)[0].min() > 0.0
+
+
+@pytest.mark.parametrize("kappa,safety,floor,cons", [(0.25, 2.5, 1e-6, 1), (0.9, 3.0, 1e-9, 0),
+                                                      (0.0, 2.0, 1e-7, 1)])
+def test_jet_lattice_parameters_bitwise(vlbm, vo, kappa, safety, floor, cons):
+    """Non-default lattice parameters of the jet (lattice.hpp:13-35): RLMP
+    relaxation kappa, the dt safety factor, the positivity floor and the
+    conservative (hypot) signal-speed bound; 60 steps of 2 samples, fields
+    and times bit-identical to the oracle."""
+    g = vlbm.Grid(200, 40)
+    lat = vlbm.LatticeParams(safety=safety, rlmp_relaxation=kappa, positivity_floor=floor,
+                             conservative_bound=bool(cons))
+    sim = vlbm.BatchSimulation.jet(g, lat, n_samples=2, base_seed=3)
+    sim.step(60)
+    t, _, _ = sim.scalars()
+    p = make_params(safety=safety, kappa=kappa, floor=floor, conservative_bound=cons)
+    for m in range(2):
+        r = vo.jet_sim(make_grid(200, 40), p, make_pert(), 3, m)
+        for _ in range(60):
+            r.step(r.suggest_dt())
+        assert bits(t[m]) == bits(r.time)
+        u, pops = r.get(pops=True)
+        assert_bitwise(sim.state(m), u, f"u sample {m}")
+        assert_bitwise(sim.populations(m), pops, f"pops sample {m}")

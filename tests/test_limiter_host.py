@@ -49,6 +49,7 @@ def test_limiter_paths_bit_exact(vo, limiter_check, tmp_path, m, steps, every):
     assert r["bisections"] > 1000  # late-time march: the bisection paths are exercised
     assert r["replay_stopped"] > 0  # ... including the tail resumption
     assert r["certified_at_one"] > 0
+    assert r["hypot_checks"] > 100000  # hypot_ref (conservative bound) == this host's libm
     for k in ("certificate_errors", "mismatch_plain", "mismatch_queued", "mismatch_replay",
-              "audit_errors", "margin_errors"):
+              "audit_errors", "margin_errors", "hypot_errors"):
         assert r[k] == 0, (k, r)
