@@ -385,3 +385,26 @@ def test_jet_lattice_parameters_bitwise(vlbm, vo, kappa, safety, floor, cons):
         u, pops = r.get(pops=True)
         assert_bitwise(sim.state(m), u, f"u sample {m}")
         assert_bitwise(sim.populations(m), pops, f"pops sample {m}")
+
+
+def test_jet_perturbation_parameters_bitwise(vlbm, vo):
+    """Non-default jet / perturbation parameters (perturbation.hpp:16-31:
+    amplitude, modes, decay, jet radius, density and speed, ambient state)
+    and inlet strip width: 50 steps of 3 samples, fields and times
+    bit-identical to the oracle."""
+    kw = dict(amplitude=0.3, modes=5, decay_exponent=1.5, r_jet=0.08, rho_jet_bar=3.0,
+              rho_amb=0.7, p_amb=0.5, v_jet=500.0)
+    g = vlbm.Grid(160, 32)
+    pp = vlbm.PerturbationParams(**kw)
+    sim = vlbm.BatchSimulation.jet(g, vlbm.LatticeParams(), vlbm.GasParams(), pp, base_seed=9,
+                                   m0=4, n_samples=3, strip_width=0.05)
+    sim.step(50)
+    t, _, _ = sim.scalars()
+    for s in range(3):
+        r = vo.jet_sim(make_grid(160, 32), make_params(), make_pert(**kw), 9, 4 + s, strip=0.05)
+        for _ in range(50):
+            r.step(r.suggest_dt())
+        assert bits(t[s]) == bits(r.time)
+        u, pops = r.get(pops=True)
+        assert_bitwise(sim.state(s), u, f"u sample {4 + s}")
+        assert_bitwise(sim.populations(s), pops, f"pops sample {4 + s}")
