@@ -408,3 +408,21 @@ def test_jet_perturbation_parameters_bitwise(vlbm, vo):
         u, pops = r.get(pops=True)
         assert_bitwise(sim.state(s), u, f"u sample {4 + s}")
         assert_bitwise(sim.populations(s), pops, f"pops sample {4 + s}")
+
+
+def test_config2_first_50_steps_bitwise(vlbm, vo):
+    """BASELINE configs[1]'s parity statement: per-sample fields of the
+    1000x200 jet equal the CPU oracle for the first 50 steps (here every bit,
+    4 of the 64 samples: 0, 21, 42, 63 of a 64-sample batch)."""
+    g = vlbm.Grid(1000, 200)
+    sim = vlbm.BatchSimulation.jet(g, n_samples=64, base_seed=42)
+    sim.step(50)
+    t, steps, _ = sim.scalars()
+    for m in (0, 21, 42, 63):
+        r = vo.jet_sim(make_grid(1000, 200), make_params(), make_pert(), 42, m)
+        for _ in range(50):
+            r.step(r.suggest_dt())
+        assert steps[m] == 50 and bits(t[m]) == bits(r.time)
+        u, pops = r.get(pops=True)
+        assert_bitwise(sim.state(m), u, f"u sample {m}")
+        assert_bitwise(sim.populations(m), pops, f"pops sample {m}")
