@@ -41,7 +41,10 @@
 #define VLBM_ADV_MINB 4  // resident advance CTAs per SM (register budget)
 #endif
 namespace vlbm_dev {
-constexpr int kCertProbe = 8;  // steps between re-probes of a warp's certificate
+#ifndef VLBM_CERT_PROBE
+#define VLBM_CERT_PROBE 32  // measured: 4 +1.5 %, 8 +1.5 %, 32 ~ 64 ~ 256 (tile pass time)
+#endif
+constexpr int kCertProbe = VLBM_CERT_PROBE;  // steps between re-probes of a warp's certificate
 namespace tiled {
 constexpr int TX = 32, TY = 8, NT = TX * TY;
 constexpr int RX2 = TX + 4, RY2 = TY + 4, NR2 = RX2 * RY2;  // limiter u box (halo 2): 36 x 12
