@@ -41,6 +41,9 @@
 #define VLBM_ADV_MINB 4  // resident advance CTAs per SM (register budget)
 #endif
 namespace vlbm_dev {
+#ifndef VLBM_CERT_TRY
+#define VLBM_CERT_TRY 2  // a warp tries the certificate while its hint is at least this
+#endif
 #ifndef VLBM_CERT_PROBE
 #define VLBM_CERT_PROBE 32  // measured: 4 +1.5 %, 8 +1.5 %, 32 ~ 64 ~ 256 (tile pass time)
 #endif
@@ -411,7 +414,7 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_THETA_MINB)
     unsigned char* hint =
         P.cert_hint ? P.cert_hint + (long long)t * 8 + (threadIdx.x >> 5) : nullptr;
     const int h0 = hint ? *hint : 3;
-    const bool try_cert = P.cert1 && (h0 >= 2 || (c->steps % kCertProbe) == 0);
+    const bool try_cert = P.cert1 && (h0 >= VLBM_CERT_TRY || (c->steps % kCertProbe) == 0);
     if (valid) {
       if (diag_ok(1.0, foC, delta, b, gm1)) {
         double parts[2] = {0.0, 0.0};
