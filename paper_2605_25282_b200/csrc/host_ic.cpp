@@ -45,9 +45,11 @@ int validate_params(const vlbm_params& p) {
     return set_error(VLBM_E_INVALID, "Simulation: walls are supported on y sides only");
   if (p.bc[1] == VLBM_BC_INLET || p.bc[1] == VLBM_BC_WALL)
     return set_error(VLBM_E_INVALID, "Simulation: unsupported x_max boundary");
-  if (p.bc[2] == VLBM_BC_INLET || p.bc[2] == VLBM_BC_OUTFLOW || p.bc[3] == VLBM_BC_INLET ||
-      p.bc[3] == VLBM_BC_OUTFLOW)
-    return set_error(VLBM_E_INVALID, "Simulation: y sides must be Wall or Periodic");
+  // y sides: a wall mirrors; any other type wraps (fill_ghosts, solver.hpp:
+  // 270-285), while only a Periodic pair makes the boundary faces periodic for
+  // interface_theta (:513) -- the reference accepts Inlet / Outflow there.
+  // The x-side rejections above surface in the reference at the first
+  // fill_ghosts (:254, :268); here already when the batch is created.
   return VLBM_OK;
 }
 

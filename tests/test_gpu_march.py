@@ -426,3 +426,52 @@ def test_config2_first_50_steps_bitwise(vlbm, vo):
         u, pops = r.get(pops=True)
         assert_bitwise(sim.state(m), u, f"u sample {m}")
         assert_bitwise(sim.populations(m), pops, f"pops sample {m}")
+
+
+MIXED_BCS = {
+    "inlet_outflow_x_inlet_as_wrap_y": (INLET, OUTFLOW, INLET, INLET),
+    "outflow_x_outflow_wrap_wall_y": (OUTFLOW, OUTFLOW, OUTFLOW, WALL),
+    "inlet_outflow_x_wall_inlet_wrap_y": (INLET, OUTFLOW, WALL, INLET),
+    "periodic_x_outflow_wrap_y": (PERIODIC, PERIODIC, OUTFLOW, OUTFLOW),
+}
+
+
+@pytest.mark.parametrize("case", list(MIXED_BCS))
+def test_mixed_boundaries_bitwise_vs_reference(vlbm, ref, case):
+    """Boundary combinations the reference accepts beyond the jet's: a y side
+    that is neither wall nor periodic wraps its ghosts (solver.hpp:274-285)
+    while its boundary faces stay non-periodic for interface_theta (:513),
+    also next to a wall on the other y side (fill_ghosts' corner order).
+    Checked against the reference itself (oracle/_ref), 25 steps."""
+    bc = MIXED_BCS[case]
+    nx, ny = 60, 12
+    pp = make_pert()
+    seed, yc, zc = ref.draw_coefficients(5, 2, 10)
+    rows = ref.inlet_rows(make_grid(nx, ny), yc, zc, pp)
+    init = ref.initial_field(make_grid(nx, ny), yc, zc, pp, strip=0.1)
+    init[0, 3, 50] *= 2.0  # something for the wraps and mirrors to carry
+    g = vlbm.Grid(nx, ny)
+    bcs = vlbm.Boundaries(*[vlbm.BcType(b) for b in bc])
+    sim = vlbm.BatchSimulation(g, vlbm.LatticeParams(), vlbm.GasParams(), bcs, init, rows)
+    r = ref.sim(make_grid(nx, ny), make_params(bc=bc), init, rows)
+    for n in (1, 24):
+        sim.step(n)
+        for _ in range(n):
+            r.step(r.suggest_dt())
+        u, p = r.get(pops=True)
+        assert_bitwise(sim.state(0), u, f"{case} u")
+        assert_bitwise(sim.populations(0), p, f"{case} pops")
+
+
+@pytest.mark.parametrize("bc", [(WALL, OUTFLOW, WALL, WALL), (INLET, INLET, WALL, WALL),
+                                (INLET, WALL, WALL, WALL)])
+def test_unsupported_x_boundaries_rejected(vlbm, bc):
+    """x walls and an x_max inlet are rejected as the reference rejects them
+    (std::invalid_argument -> ValueError), before any march."""
+    g = vlbm.Grid(16, 4)
+    init = np.zeros((4, 4, 16))
+    init[0], init[3] = 1.0, 1.0
+    bcs = vlbm.Boundaries(*[vlbm.BcType(b) for b in bc])
+    with pytest.raises(ValueError):
+        vlbm.BatchSimulation(g, vlbm.LatticeParams(), vlbm.GasParams(), bcs, init,
+                             np.ones((4, 4)))
