@@ -475,3 +475,28 @@ def test_unsupported_x_boundaries_rejected(vlbm, bc):
     with pytest.raises(ValueError):
         vlbm.BatchSimulation(g, vlbm.LatticeParams(), vlbm.GasParams(), bcs, init,
                              np.ones((4, 4)))
+
+
+@pytest.mark.parametrize("alpha", [0.5, 0.9])
+def test_rest_population_weight_bitwise(vlbm, vo, alpha):
+    """alpha in (0, 1) (test_lattice.cpp:31-49: M5 = alpha u, w = (1 - alpha)/4):
+    periodic smooth field with a spike, RLMP, 10 steps bit-identical to the
+    oracle.  (With this spike alpha = 0.9 becomes inadmissible at step 14 and
+    alpha = 1 at step 11; the batch then stops the sample as run_sample does,
+    while a bare Simulation::step keeps stepping NaNs.)"""
+    nx, ny = 32, 16
+    x_max = 0.5 * nx / ny
+    init = smooth_field(nx, ny, x_max)
+    init[0, 5, 7] *= 2.5
+    bc = (PERIODIC, PERIODIC, PERIODIC, PERIODIC)
+    g = vlbm.Grid(nx, ny, x_max)
+    lat = vlbm.LatticeParams(alpha=alpha)
+    bcs = vlbm.Boundaries(*[vlbm.BcType(b) for b in bc])
+    sim = vlbm.BatchSimulation(g, lat, vlbm.GasParams(1.4), bcs, init)
+    r = vo.sim(make_grid(nx, ny, x_max), make_params(gamma=1.4, alpha=alpha, bc=bc), init)
+    sim.step(10)
+    for _ in range(10):
+        r.step(r.suggest_dt())
+    u, p = r.get(pops=True)
+    assert_bitwise(sim.state(0), u, f"alpha {alpha} u")
+    assert_bitwise(sim.populations(0), p, f"alpha {alpha} pops")
