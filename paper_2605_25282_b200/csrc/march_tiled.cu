@@ -664,6 +664,9 @@ __device__ __forceinline__ void load_unc_entry(const MarchParams& P, int s, long
 constexpr int kReplayInline = VLBM_REPLAY_INLINE;
 
 // blockIdx.y = cq bin; bins run concurrently.
+#ifndef VLBM_UNC_GRID
+#define VLBM_UNC_GRID 2  // k_bisect_unc CTAs per bin = 148 x this (measured: 1, 3, 6 slower)
+#endif
 #ifndef VLBM_UNC_MINB
 #define VLBM_UNC_MINB 2
 #endif
@@ -946,7 +949,7 @@ cudaError_t launch_theta_hard(const MarchParams& P, cudaStream_t st) {
   if (P.hq) {
     k_theta_hard<<<148 * 2, 256, kHardSmem, st>>>(P);
     k_bisect_cert<<<148 * 8, 256, 0, st>>>(P);
-    k_bisect_unc<<<dim3(148 * 3, 3), 256, 0, st>>>(P);
+    k_bisect_unc<<<dim3(148 * VLBM_UNC_GRID, 3), 256, 0, st>>>(P);
     if (P.replay) k_bisect_tail<<<148 * 4, 128, 0, st>>>(P);
   }
   return cudaGetLastError();
