@@ -70,6 +70,7 @@ struct vlbm_batch {
   int* d_active_g = nullptr;
   int* h_active_g = nullptr;     // pinned
   cudaEvent_t ev_fork = nullptr;
+  bool graphs = true;  // chunks after the first replay as a CUDA graph (VLBM_GRAPHS=0: off)
 };
 
 namespace {
@@ -202,6 +203,7 @@ int alloc_batch(const vlbm_grid* g, const vlbm_params* p, int S, int device, vlb
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   if (const char* e = getenv("VLBM_GROUPS")) G = std::max(1, std::min(S, atoi(e)));
   b->G = G;
+  if (const char* e = getenv("VLBM_GRAPHS")) b->graphs = atoi(e) != 0;
   chk(cudaMalloc(&b->d_active_g, sizeof(int) * G), "malloc active_g");
   chk(cudaMallocHost(&b->h_active_g, sizeof(int) * G), "malloc host active_g");
   chk(cudaEventCreateWithFlags(&b->ev_fork, cudaEventDisableTiming), "event");
@@ -340,11 +342,11 @@ int march_loop(vlbm_batch* b, double target, double fixed_dt, int mode, int chun
   const int adv_mode = mode == 2 ? 2 : (rlmp ? 0 : 1);
   const double const_theta = b->p.limiter == VLBM_LIMITER_SECOND_ORDER ? 1.0 : 0.0;
   const int G = b->G;
-  for (;;) {
+  auto issue = [&](int n) -> int {
     // fork: the group streams start after everything queued on the main stream
-    CU(cudaEventRecord(b->ev_fork, b->stream));
+    if (G > 1) CU(cudaEventRecord(b->ev_fork, b->stream));
     for (int g = 1; g < G; ++g) CU(cudaStreamWaitEvent(b->sg[g], b->ev_fork, 0));
-    for (int it = 0; it < chunk; ++it) {
+    for (int it = 0; it < n; ++it) {
       for (int g = 0; g < G; ++g) {  // groups interleaved: their kernels overlap
         const MarchParams& Q = b->Pg[g];
         cudaStream_t st = b->sg[g];
@@ -365,16 +367,74 @@ int march_loop(vlbm_batch* b, double target, double fixed_dt, int mode, int chun
         b->launches += rlmp ? (Q.hq ? (Q.replay ? 7 : 6) : 3) : 2;
       }
     }
-    for (int g = 0; g < G; ++g)
-      CU(cudaMemcpyAsync(b->h_active_g + g, b->Pg[g].n_active, sizeof(int),
-                         cudaMemcpyDeviceToHost, b->sg[g]));
-    for (int g = 0; g < G; ++g) CU(cudaStreamSynchronize(b->sg[g]));
+    return VLBM_OK;
+  };
+  // From the second chunk of a call on, the chunk's launches replay as one
+  // CUDA graph (captured once per call: the kernel arguments are fixed for
+  // the call, the per-step state lives on the device). Not while per-launch
+  // timing is on (its events are harvested on the host) or with several
+  // sample groups.
+  const bool use_graph = b->graphs && !b->timing && G == 1;
+  cudaGraphExec_t exec = nullptr;
+  int exec_chunk = -1;
+  long long exec_launches = 0;
+  int rc = VLBM_OK;
+  for (int pass = 0;; ++pass) {
+    if (use_graph && pass > 0) {
+      if (exec_chunk != chunk) {
+        if (exec) cudaGraphExecDestroy(exec);
+        exec = nullptr;
+        const long long l0 = b->launches;
+        cudaGraph_t graph = nullptr;
+        cudaError_t e = cudaStreamBeginCapture(b->stream, cudaStreamCaptureModeThreadLocal);
+        if (e != cudaSuccess) {
+          rc = set_error(VLBM_E_CUDA, std::string("cudaStreamBeginCapture: ") + cudaGetErrorString(e));
+          break;
+        }
+        const int ri = issue(chunk);
+        e = cudaStreamEndCapture(b->stream, &graph);
+        if (ri != VLBM_OK) {
+          if (graph) cudaGraphDestroy(graph);
+          rc = ri;
+          break;
+        }
+        if (e == cudaSuccess) e = cudaGraphInstantiate(&exec, graph, 0);
+        if (graph) cudaGraphDestroy(graph);
+        if (e != cudaSuccess) {
+          exec = nullptr;
+          rc = set_error(VLBM_E_CUDA, std::string("CUDA graph capture: ") + cudaGetErrorString(e));
+          break;
+        }
+        exec_launches = b->launches - l0;
+        b->launches = l0;
+        exec_chunk = chunk;
+      }
+      cudaError_t e = cudaGraphLaunch(exec, b->stream);
+      if (e != cudaSuccess) {
+        rc = set_error(VLBM_E_CUDA, std::string("cudaGraphLaunch: ") + cudaGetErrorString(e));
+        break;
+      }
+      b->launches += exec_launches;
+    } else if ((rc = issue(chunk)) != VLBM_OK) {
+      break;
+    }
+    cudaError_t e = cudaSuccess;
+    for (int g = 0; g < G && e == cudaSuccess; ++g)
+      e = cudaMemcpyAsync(b->h_active_g + g, b->Pg[g].n_active, sizeof(int),
+                          cudaMemcpyDeviceToHost, b->sg[g]);
+    for (int g = 0; g < G && e == cudaSuccess; ++g) e = cudaStreamSynchronize(b->sg[g]);
+    if (e != cudaSuccess) {
+      rc = set_error(VLBM_E_CUDA, std::string("march poll: ") + cudaGetErrorString(e));
+      break;
+    }
     if (b->timing) harvest(b);
     int active = 0;
     for (int g = 0; g < G; ++g) active += b->h_active_g[g];
-    if (active == 0) return VLBM_OK;
+    if (active == 0) break;
     if (mode == 2) chunk = 1;
   }
+  if (exec) cudaGraphExecDestroy(exec);
+  return rc;
 }
 
 int read_ctl(vlbm_batch* b, std::vector<SampleCtl>& ctl) {

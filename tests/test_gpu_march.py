@@ -500,3 +500,35 @@ def test_rest_population_weight_bitwise(vlbm, vo, alpha):
     u, p = r.get(pops=True)
     assert_bitwise(sim.state(0), u, f"alpha {alpha} u")
     assert_bitwise(sim.populations(0), p, f"alpha {alpha} pops")
+
+
+@pytest.mark.parametrize("limiter", [RLMP, FIRST_ORDER])
+def test_graph_replay_matches_direct_launches(vlbm, vo, monkeypatch, limiter):
+    """Chunks after a call's first replay as one captured CUDA graph
+    (capi.cu march_loop).  With graphs off (VLBM_GRAPHS=0) the same calls --
+    run_to over many chunks, two targets, then step(n) -- give identical
+    bits, step counts and launch counts; both match the oracle."""
+    g = vlbm.Grid(200, 40)
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("VLBM_GRAPHS", flag)
+        sim = vlbm.BatchSimulation.jet(g, vlbm.LatticeParams(limiter=vlbm.Limiter(limiter)),
+                                       n_samples=3, base_seed=42)
+        sim.run_to(0.0003)
+        sim.run_to(0.0005)
+        sim.step(37)
+        out[flag] = ([sim.state(m) for m in range(3)], sim.scalars()[1].copy(),
+                     sim.stats()["launches"])
+        sim.close()
+    for m in range(3):
+        assert_bitwise(out["1"][0][m], out["0"][0][m], f"graph vs direct sample {m}")
+    assert list(out["1"][1]) == list(out["0"][1])
+    assert out["1"][2] == out["0"][2]
+    r = vo.jet_sim(make_grid(200, 40), make_params(limiter=limiter), make_pert(), 42, 2)
+    for target in (0.0003, 0.0005):
+        while r.time < target - 1e-12:
+            r.step(min(r.suggest_dt(), target - r.time))
+    for _ in range(37):
+        r.step(r.suggest_dt())
+    assert out["1"][1][2] == r.steps
+    assert_bitwise(out["1"][0][2], r.get(), "graph replay vs oracle")
