@@ -944,13 +944,19 @@ int theta_ctas_per_sm() {
   return n > 0 ? n : 1;
 }
 
+#ifndef VLBM_CERT_GRID
+#define VLBM_CERT_GRID 8  // k_bisect_cert CTAs = 148 x this
+#endif
+#ifndef VLBM_TAIL_GRID
+#define VLBM_TAIL_GRID 4  // k_bisect_tail CTAs = 148 x this
+#endif
 cudaError_t launch_theta_hard(const MarchParams& P, cudaStream_t st) {
   if (cudaError_t e = smem_attrs()) return e;
   if (P.hq) {
     k_theta_hard<<<148 * 2, 256, kHardSmem, st>>>(P);
-    k_bisect_cert<<<148 * 8, 256, 0, st>>>(P);
+    k_bisect_cert<<<148 * VLBM_CERT_GRID, 256, 0, st>>>(P);
     k_bisect_unc<<<dim3(148 * VLBM_UNC_GRID, 3), 256, 0, st>>>(P);
-    if (P.replay) k_bisect_tail<<<148 * 4, 128, 0, st>>>(P);
+    if (P.replay) k_bisect_tail<<<148 * VLBM_TAIL_GRID, 128, 0, st>>>(P);
   }
   return cudaGetLastError();
 }
