@@ -70,6 +70,7 @@ struct vlbm_batch {
   int* d_active_g = nullptr;
   int* h_active_g = nullptr;     // pinned
   cudaEvent_t ev_fork = nullptr;
+  bool cert_side = true;  // k_bisect_cert on a side stream (VLBM_CERT_SIDE=0: in line)
   bool graphs = true;  // chunks after the first replay as a CUDA graph (VLBM_GRAPHS=0: off)
 };
 
@@ -104,6 +105,11 @@ void free_batch(vlbm_batch* b) {
     cudaFree(Q.hq_n);
     cudaFree(Q.bq);
     cudaFree(Q.bq_idx);
+    cudaFree(Q.tq);
+    cudaFree(Q.tq_idx);
+    if (Q.side) cudaStreamDestroy(Q.side);
+    if (Q.ev_fork) cudaEventDestroy(Q.ev_fork);
+    if (Q.ev_join) cudaEventDestroy(Q.ev_join);
     cudaFree(Q.cq);
     cudaFree(Q.cq_idx);
     if (g > 0 && b->sg[g]) cudaStreamDestroy(b->sg[g]);
@@ -204,6 +210,7 @@ int alloc_batch(const vlbm_grid* g, const vlbm_params* p, int S, int device, vlb
   if (const char* e = getenv("VLBM_GROUPS")) G = std::max(1, std::min(S, atoi(e)));
   b->G = G;
   if (const char* e = getenv("VLBM_GRAPHS")) b->graphs = atoi(e) != 0;
+  if (const char* e = getenv("VLBM_CERT_SIDE")) b->cert_side = atoi(e) != 0;
   chk(cudaMalloc(&b->d_active_g, sizeof(int) * G), "malloc active_g");
   chk(cudaMallocHost(&b->h_active_g, sizeof(int) * G), "malloc host active_g");
   chk(cudaEventCreateWithFlags(&b->ev_fork, cudaEventDisableTiming), "event");
@@ -211,7 +218,7 @@ int alloc_batch(const vlbm_grid* g, const vlbm_params* p, int S, int device, vlb
   // (overflowing CTAs finish their hard cells in place).
   const size_t entry =
       sizeof(double) * (vlbm_dev::kHardWords + vlbm_dev::kBisWords + vlbm_dev::kUncWords) +
-      3 * sizeof(long long);
+      4 * sizeof(long long) + 2 * sizeof(double);
   const size_t avail =
       free_b > need + (size_t)(2ull << 30) ? free_b - need - (size_t)(2ull << 30) : 0;
   for (int g = 0; g < G && rc == VLBM_OK; ++g) {
@@ -242,6 +249,13 @@ int alloc_batch(const vlbm_grid* g, const vlbm_params* p, int S, int device, vlb
         chk(cudaMalloc(&Q.hq_idx, sizeof(long long) * cap), "malloc hq_idx");
         chk(cudaMalloc(&Q.bq, sizeof(double) * vlbm_dev::kBisWords * cap), "malloc bq");
         chk(cudaMalloc(&Q.bq_idx, sizeof(long long) * cap), "malloc bq_idx");
+        chk(cudaMalloc(&Q.tq, sizeof(double) * 2 * cap), "malloc tq");
+        chk(cudaMalloc(&Q.tq_idx, sizeof(long long) * cap), "malloc tq_idx");
+        if (b->cert_side) {
+          chk(cudaStreamCreateWithFlags(&Q.side, cudaStreamNonBlocking), "stream side");
+          chk(cudaEventCreateWithFlags(&Q.ev_fork, cudaEventDisableTiming), "event");
+          chk(cudaEventCreateWithFlags(&Q.ev_join, cudaEventDisableTiming), "event");
+        }
         chk(cudaMalloc(&Q.cq, sizeof(double) * vlbm_dev::kUncWords * cap), "malloc cq");
         chk(cudaMalloc(&Q.cq_idx, sizeof(long long) * cap), "malloc cq_idx");
         // counters: [0] hard cells, [2] bq, [3..5] cq bins, [6] limiter tile claims

@@ -65,12 +65,16 @@ struct MarchParams {
   int hq_cap;
   // Bisection queues (capacity hq_cap each), filled by k_theta_hard:
   //   bq: vertices all certified -- u_FO(4), delta(4), rho_lo/hi, p_lo/hi, thc  (kBisWords);
-  //       after k_bisect_cert (replay on) it holds the bisections k_bisect_unc
-  //       stopped: lo, hi in words 0, 1; bq_idx = cq slot | step << 40 (count hq_n[7])
   //   cq: some uncertified -- u_FO(4), c_f(16), rho_lo/hi, p_lo/hi, thc, p0, err, er (kUncWords)
   //   *_idx: cell index; cq_idx packs the uncertified-vertex mask in bits 40..55
   double* bq;
   long long* bq_idx;
+  // Tail queue of k_bisect_unc (its own storage, so k_bisect_cert can run
+  // beside it): lo, hi (2 x hq_cap doubles); tq_idx = cq slot | step << 40.
+  double* tq;
+  long long* tq_idx;
+  cudaStream_t side;               // k_bisect_cert's stream (joined before the advance)
+  cudaEvent_t ev_fork, ev_join;    // fork after k_theta_hard / join after k_bisect_cert
   double* cq;
   long long* cq_idx;
   int* audit;    // optional: disagreements of the certified bisection (must stay 0)

@@ -699,16 +699,16 @@ __global__ void __launch_bounds__(256, VLBM_UNC_MINB) k_bisect_unc(MarchParams P
     const int t = warp_slot(stopped, P.hq_n + 7, &tbase, &nt);
     if (stopped) {
       if (tbase + nt <= P.hq_cap) {
-        P.bq[t] = br.lo;
-        P.bq[cap + t] = br.hi;
-        P.bq_idx[t] = (long long)s | ((long long)br.it << 40);
+        P.tq[t] = br.lo;
+        P.tq[cap + t] = br.hi;
+        P.tq_idx[t] = (long long)s | ((long long)br.it << 40);
       } else {  // tail full: finish here
         cs fo, cf[4];
         RlmpBounds b;
         HardStage h;
         load_unc_entry(P, s, packed, fo, cf, b, h);
         const cs delta = add(add(cf[0], cf[1]), add(cf[2], cf[3]));
-        if (t < P.hq_cap) P.bq_idx[t] = -1;
+        if (t < P.hq_cap) P.tq_idx[t] = -1;
         P.theta[packed & kIdxMask] = bisect_finish(fo, cf, delta, b, h.unc, br, P.gm1, P.audit);
       }
     }
@@ -720,7 +720,7 @@ __global__ void __launch_bounds__(128, 4) k_bisect_tail(MarchParams P) {
   const int n = min(P.hq_n[7], P.hq_cap);
   const long long cap = P.hq_cap;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
-    const long long tp = P.bq_idx[t];
+    const long long tp = P.tq_idx[t];
     if (tp < 0) continue;
     const int s = (int)(tp & kIdxMask);
     const long long packed = P.cq_idx[s];
@@ -729,8 +729,8 @@ __global__ void __launch_bounds__(128, 4) k_bisect_tail(MarchParams P) {
     HardStage h;
     load_unc_entry(P, s, packed, fo, cf, b, h);
     const cs delta = add(add(cf[0], cf[1]), add(cf[2], cf[3]));
-    P.theta[packed & kIdxMask] = bisect_uncertified(fo, cf, delta, b, h, P.gm1, P.audit, P.bq[t],
-                                                    P.bq[cap + t], (int)(tp >> 40));
+    P.theta[packed & kIdxMask] = bisect_uncertified(fo, cf, delta, b, h, P.gm1, P.audit, P.tq[t],
+                                                    P.tq[cap + t], (int)(tp >> 40));
   }
 }
 
@@ -954,9 +954,23 @@ cudaError_t launch_theta_hard(const MarchParams& P, cudaStream_t st) {
   if (cudaError_t e = smem_attrs()) return e;
   if (P.hq) {
     k_theta_hard<<<148 * 2, 256, kHardSmem, st>>>(P);
-    k_bisect_cert<<<148 * VLBM_CERT_GRID, 256, 0, st>>>(P);
+    // the certified (diagonal-only) bisections run beside the uncertified
+    // ones: disjoint cells and queues; joined before the advance
+    cudaStream_t cs_ = st;
+    if (P.side) {
+      if (cudaError_t e = cudaEventRecord(P.ev_fork, st)) return e;
+      if (cudaError_t e = cudaStreamWaitEvent(P.side, P.ev_fork, 0)) return e;
+      cs_ = P.side;
+    }
+    k_bisect_cert<<<148 * VLBM_CERT_GRID, 256, 0, cs_>>>(P);
+    if (P.side) {
+      if (cudaError_t e = cudaGetLastError()) return e;
+      if (cudaError_t e = cudaEventRecord(P.ev_join, P.side)) return e;
+    }
     k_bisect_unc<<<dim3(148 * VLBM_UNC_GRID, 3), 256, 0, st>>>(P);
     if (P.replay) k_bisect_tail<<<148 * VLBM_TAIL_GRID, 128, 0, st>>>(P);
+    if (P.side)
+      if (cudaError_t e = cudaStreamWaitEvent(st, P.ev_join, 0)) return e;
   }
   return cudaGetLastError();
 }
