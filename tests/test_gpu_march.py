@@ -532,3 +532,25 @@ def test_graph_replay_matches_direct_launches(vlbm, vo, monkeypatch, limiter):
         r.step(r.suggest_dt())
     assert out["1"][1][2] == r.steps
     assert_bitwise(out["1"][0][2], r.get(), "graph replay vs oracle")
+
+
+def test_cert_side_stream_matches_in_line(vlbm, vo, monkeypatch):
+    """k_bisect_cert on its side stream (default) and in line on the main
+    stream (VLBM_CERT_SIDE=0) give the same bits at late time, where all
+    three bisection kernels have work; both match the oracle."""
+    g = vlbm.Grid(200, 40)
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("VLBM_CERT_SIDE", flag)
+        sim = vlbm.BatchSimulation.jet(g, n_samples=4, base_seed=42)
+        sim.run_to(0.0008)
+        out[flag] = ([sim.state(m) for m in range(4)], sim.scalars()[1].copy())
+        sim.close()
+    for m in range(4):
+        assert_bitwise(out["1"][0][m], out["0"][0][m], f"side vs in-line sample {m}")
+    assert list(out["1"][1]) == list(out["0"][1])
+    r = vo.jet_sim(make_grid(200, 40), make_params(), make_pert(), 42, 1)
+    while r.time < 0.0008 - 1e-12:
+        r.step(min(r.suggest_dt(), 0.0008 - r.time))
+    assert out["1"][1][1] == r.steps
+    assert_bitwise(out["1"][0][1], r.get(), "side stream vs oracle")
