@@ -37,9 +37,20 @@ sys.path.insert(0, ROOT)
 NX, NY, M_PER_GPU = 1000, 200, 64
 BYTES_PER_UPDATE = 320      # read u(4)+pops(16) f64, write the same
 THETA_BYTES_PER_CELL = 168  # k_theta_tiled: read u + pops (160 B), write theta (8 B)
-# FP64 peak of the non-tensor pipe, counting DADD/DMUL/DFMA as one instruction
-# (the march is built with --fmad=false): 148 SMs x 64 FP64 lanes x 1.965 GHz.
-FP64_PEAK_TINST = 148 * 64 * 1.965e9 / 1e12
+# FP64 peak of the non-tensor pipe, counting DADD/DMUL/DFMA as one
+# instruction (the march is built with --fmad=false): measured by
+# tools/fp64_peak.cu (profiles/fp64_peak.json, DADD/DMUL/DFMA instructions/s,
+# the best of the three); fallback 148 SMs x 64 FP64 lanes x 1.965 GHz.
+FP64_PEAK_THEORY = 148 * 64 * 1.965e9 / 1e12
+
+
+def fp64_peak():
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as f:
+            d = json.load(f)
+        return max(d["dadd_per_s"], d["dmul_per_s"], d["dfma_per_s"]) / 1e12, "measured"
+    except Exception:
+        return FP64_PEAK_THEORY, "theoretical"
 
 
 def peaks():
@@ -119,40 +130,87 @@ def dist_env():
     return ws, rank, local
 
 
-def cpu_reference(args, n_gpus, threads=None, seconds=None):
-    seconds = seconds or getattr(args, "ref_seconds", 15.0)
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def cpu_reference(args, n_gpus, threads=None, seconds=None, max_steps=None):
     """The reference CPU march (oracle/_ref = the unmodified reference
-    headers) on this host's cores: one sample per thread, run_ensemble-style
-    task pool, file I/O excluded; a bounded sample of the same workload
-    (1000x200 jet samples, the first `steps` VLBM steps of each)."""
+    headers) on this host's cores, one sample per thread (run_ensemble's
+    worker pool minus file I/O), on the SAME window the GPU arm times: every
+    sample marched untimed to --t-start with run_sample's loop, then a bounded
+    number of steps timed (about `seconds` of CPU work)."""
+    seconds = seconds or getattr(args, "ref_seconds", 15.0)
     from oracle import oracle
     threads = threads or os.cpu_count() or 1
     kind = "reference" if oracle.available("ref") else "port"
     o = oracle.Oracle("ref" if kind == "reference" else "vo")
     g, p, pp = oracle.make_grid(NX, NY), oracle.make_params(), oracle.make_pert()
+    n_samples = min(args.samples, threads)
+    # ~2e6 updates/s per core mid-run (survey: 1.3-1.4e6 averaged to t = 0.003)
+    steps = max(2, int(seconds * 2.0e6 / (NX * NY)))
+    if max_steps:
+        steps = max(2, min(steps, max_steps))
+    pre = 0.0
     if kind == "reference":
-        # calibrate: ~1.4e6 updates/s/core measured in the survey; aim for `seconds`
-        n_samples = min(M_PER_GPU, threads)
-        steps = max(2, int(seconds * 1.4e6 * min(threads, n_samples) / (n_samples * NX * NY)))
-        sec, upd = o.march_timed(g, p, pp, 42, 0, n_samples, steps, 0.0, 0.02, threads)
-    else:
+        sec, upd, pre = o.march_window(g, p, pp, 42, 0, n_samples, args.t_start, steps, 0.02,
+                                       threads)
+    else:  # the C restatement (only when the reference could not be built)
         import concurrent.futures as cf
-        n_samples, steps = min(M_PER_GPU, threads), 5
 
         def one(m):
             s = o.jet_sim(g, p, pp, 42, m)
+            while s.time < args.t_start - 1e-12:
+                s.step(min(s.suggest_dt(), args.t_start - s.time))
+            return s
+
+        with cf.ThreadPoolExecutor(threads) as ex:
+            sims = list(ex.map(one, range(n_samples)))
+
+        def run(s):
             for _ in range(steps):
                 s.step(s.suggest_dt())
             return steps * NX * NY
 
         t0 = time.perf_counter()
         with cf.ThreadPoolExecutor(threads) as ex:
-            upd = sum(ex.map(one, range(n_samples)))
+            upd = sum(ex.map(run, sims))
         sec = time.perf_counter() - t0
     used = min(threads, n_samples)
     return {"value": upd / sec, "unit": "sample-cell-updates/s", "cores": used, "kind": kind,
-            "sample": f"{n_samples} jet samples x first {steps} steps at {NX}x{NY} "
+            "cpu_model": cpu_model(), "host_threads": os.cpu_count(),
+            "sample": f"{n_samples} jet samples at {NX}x{NY}, each marched untimed to "
+                      f"t={args.t_start:g} ({pre:.0f} s), then {steps} timed steps "
                       f"({upd:.3g} updates, {sec:.1f} s wall, {used} threads)"}
+
+
+def postproc_cpu_baseline(M=1000, nxc=2000, rows=2):
+    """The reference's restrict_field + wasserstein1 + strong_error
+    (compute_metrics' calls, single-threaded as the reference runs them) on a
+    configs[3] slice: `rows` coarse rows of 2000x400 (and the 2*rows fine rows
+    of 4000x800), M = 1000 log-normal density samples (other components 0)."""
+    import numpy as np
+    from oracle import oracle
+    if not oracle.available("ref"):
+        return None
+    rng = np.random.default_rng(3)
+    coarse = np.zeros((M, 4, rows, nxc))
+    fine = np.zeros((M, 4, 2 * rows, 2 * nxc))
+    coarse[:, 0] = rng.lognormal(-0.125, 0.5, size=(M, rows, nxc))
+    fine[:, 0] = rng.lognormal(-0.125, 0.5, size=(M, 2 * rows, 2 * nxc))
+    sec, w1, es = oracle.Oracle("ref").postproc_timed(coarse, fine)
+    nc = rows * nxc
+    return {"value": nc / sec, "unit": "coarse cells/s (W1 + L1 + restriction, M=1000)",
+            "cores": 1, "kind": "reference", "cpu_model": cpu_model(),
+            "sample": f"{rows} coarse rows x {nxc} ({nc} cells), M={M}: restrict_field of "
+                      f"the fine ensemble + wasserstein1 + strong_error in {sec:.2f} s"}
 
 
 def postproc_bench(torch, dev, M=1000, nxc=2000, nyc=400, reps=3):
@@ -310,8 +368,9 @@ METRIC = "VLBM sample-cell updates/s (GLUPS) & % HBM roofline; W1 post-proc cell
 def workload_config(args, M, ws):
     """The config object of both arms (same workload, metric and unit)."""
     return {"workload": f"{'C2 ' if (NX, NY) == (1000, 200) else ''}jet {NX}x{NY}, "
-                        f"M={M}/GPU, RLMP, fp64, steps "
-                        f"{args.warmup}..{args.warmup + args.steps} of each sample",
+                        f"M={M}/GPU, RLMP, fp64, {args.steps} steps of each sample "
+                        f"after run_to(t={args.t_start:g}) + {args.warmup} warm-up steps",
+            "t_start": args.t_start,
             "nx": NX, "ny": NY, "samples_per_gpu": M, "parallelism": f"samples/{ws}",
             "l2": f"inputs larger than L2 ({2 * 20 * 8 * M * NX * NY / 1e9:.1f} GB "
                   "state per GPU)"}
@@ -321,7 +380,7 @@ def run_reference_arm(args):
     ws, rank, local = dist_env()
     if rank != 0:
         return 0
-    cb = cpu_reference(args, ws)
+    cb = cpu_reference(args, ws, max_steps=args.steps)
     line = {"impl": "reference", "metric": METRIC,
             "value": cb["value"], "unit": "sample-cell-updates/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
@@ -335,17 +394,49 @@ def run_reference_arm(args):
     return 0
 
 
+def free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def spawn_ranks(args) -> int:
+    """--gpus N without a launcher: re-run this script under
+    torch.distributed.run with N ranks on this node (rank r on cuda:r,
+    rendezvous on 127.0.0.1); rank 0 prints the line.  On a box with fewer
+    GPUs than N (a test of the multi-rank path) the ranks share the GPUs
+    round-robin over gloo, and the line says so."""
+    env = dict(os.environ)
+    try:
+        import torch
+        ngpu = torch.cuda.device_count()
+    except Exception:
+        ngpu = 0
+    if ngpu < args.gpus:
+        env.setdefault("VLBM_BENCH_BACKEND", "gloo")
+        print(f"bench.py: {args.gpus} ranks on {ngpu} GPU(s): ranks share GPUs, backend "
+              f"{env['VLBM_BENCH_BACKEND']}", file=sys.stderr)
+    env.setdefault("NCCL_DEBUG", "INFO")  # NCCL's init lines (ranks, transports) on stderr
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    # default: steps 5..2005 of every sample, i.e. nearly the whole configs[1]
-    # run to t = 0.001 (2207 steps for sample 0), where the limiter's work grows
-    ap.add_argument("--steps", type=int, default=2000)
+    # default window: 200 steps of every sample from t = 0.0005, the middle
+    # of configs[1]'s run to t = 0.001 (the limiter's work grows with time, so
+    # the first steps would overstate the run's rate)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--samples", type=int, default=M_PER_GPU)
-    ap.add_argument("--t-start", type=float, default=0.0,
-                    help="march every sample to this time (untimed) before the warmup")
+    ap.add_argument("--t-start", type=float, default=0.0005,
+                    help="march every sample to this time (untimed, run_sample's loop) "
+                         "before the warmup")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-postproc", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -358,17 +449,24 @@ def main():
                     help="omit the roofline objects")
     ap.add_argument("--ref-seconds", type=float, default=15.0,
                     help="target CPU seconds of the reference-CPU sample")
+    ap.add_argument("--no-first-order", action="store_true",
+                    help="skip the theta = 0 (Limiter::FirstOrder) march line")
     args = ap.parse_args()
     global NX, NY
     if args.grid:
         NX, NY = (int(x) for x in args.grid.lower().split("x"))
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
 
     import numpy as np
     import torch
 
     ws, rank, local = dist_env()
+    if ws != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}", file=sys.stderr)
+        return 2
     # one GPU per rank; on a box with fewer GPUs than ranks (a test of the
     # multi-rank path only) ranks share them round-robin
     local = local % max(1, torch.cuda.device_count())
@@ -441,34 +539,43 @@ def main():
     # ---- e2e through the public API from host buffers ----
     e2e = None
     if not args.no_e2e:
-        # The user's call sequence: build the batch from the seeds (host IC
-        # through libm, H2D of the initial fields and inlet rows), march K
-        # steps, read every sample's final field back to host memory.
+        # The user's call sequence, all inside the timed region: build the
+        # batch from the seeds (host inlet rows through the reference's libm,
+        # H2D of the rows, initial field laid out on the device), run_sample's
+        # loop to t_start, the warm-up and timed steps, then every sample's
+        # final field read back into pinned host memory.  Every cell update of
+        # the call counts (the early steps included).
         out = torch.empty((M, 4, NY, NX), dtype=torch.float64).pin_memory().numpy()
         barrier()
         t0 = time.perf_counter()
         e = v.BatchSimulation.jet(g, lat, gas, pp, base_seed=42, m0=rank * M, n_samples=M,
                                   device=local)
-        e.step(args.steps)
+        if args.t_start > 0:
+            e.run_to(args.t_start)
+        e.step(args.warmup + args.steps)
         v.vlbm._check(v.lib().vlbm_batch_get_fields(e._h, v.vlbm._dp(out)))
         t1 = time.perf_counter()
         barrier()
         st = e.stats()
         e.close()
         et = t1 - t0
+        upd_e = st["cell_updates"]
         if ws > 1:
-            et = reduce_max(et)
-        h2d = M * (4 * NX * NY + 4 * NY) * 8
-        e2e = {"value": st["cell_updates"] * ws / et, "unit": "sample-cell-updates/s",
-               "h2d_bytes_per_step": int(h2d / args.steps),
-               "d2h_bytes_per_step": int(out.nbytes / args.steps),
-               "note": "BatchSimulation.jet (host IC + H2D) + K steps + D2H of all fields"}
+            et, upd_e = reduce_max(et), reduce_sum(upd_e)
+        steps_e = st["cell_updates"] / (M * NX * NY)  # per-sample steps (mean) of the call
+        h2d = M * (4 * NY * 8 + 10 * 2 * 8) + 4 * NY  # inlet rows + mode coefficients, counts
+        e2e = {"value": upd_e / et, "unit": "sample-cell-updates/s",
+               "h2d_bytes_per_step": int(h2d / steps_e),
+               "d2h_bytes_per_step": int(out.nbytes / steps_e),
+               "seconds": et, "steps_per_sample": steps_e,
+               "note": "BatchSimulation.jet (IC) + run_to(t_start) + warmup + K steps + D2H of "
+                       "every final field, wall clock; all cell updates of the call"}
 
     # ---- late-time window: the same march timed from t = 0.002, where the
     # jet is developed and ~28 % of the cells are limiter hard cells (the
     # regime of most of configs[2]'s run to t = 0.003) ----
     late = None
-    if not args.no_late and args.t_start == 0.0:
+    if not args.no_late and args.t_start < 0.002:
         lt = v.BatchSimulation.jet(g, lat, gas, pp, base_seed=42, m0=rank * M, n_samples=M,
                                    device=local)
         lt.run_to(0.002)
@@ -496,6 +603,45 @@ def main():
                 "kernel_ms_per_step": {k: (l1[k] - l0[k]) / args.late_steps for k in
                                        ("ms_theta_tiles", "ms_theta_hard", "ms_advance",
                                         "ms_sched")}}
+
+    # ---- theta = 0 (Limiter::FirstOrder, lattice.hpp:10, solver.hpp:492-495):
+    # the same march without the limiter -- the collide+stream kernel alone,
+    # the HBM-roofline demonstration of BASELINE.md §3 ----
+    fo_line = None
+    if not args.no_first_order:
+        lat0 = v.LatticeParams(limiter=v.Limiter.FirstOrder)
+        f0 = v.BatchSimulation.jet(g, lat0, gas, pp, base_seed=42, m0=rank * M, n_samples=M,
+                                   device=local)
+        if args.t_start > 0:
+            f0.run_to(args.t_start)
+        f0.step(args.warmup)
+        f0.set_timing(True)
+        a0 = f0.stats()
+        barrier()
+        fstream = torch.cuda.ExternalStream(f0.stream(), device=torch.device("cuda", local))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(fstream)
+        f0.step(args.steps)
+        e1.record(fstream)
+        torch.cuda.synchronize()
+        barrier()
+        a1 = f0.stats()
+        f0.close()
+        fms = e0.elapsed_time(e1)
+        fupd = a1["cell_updates"] - a0["cell_updates"]
+        adv_ms = (a1["ms_advance"] - a0["ms_advance"]) / args.steps
+        if ws > 1:
+            fms, fupd = reduce_max(fms), reduce_sum(fupd)
+        hbm0, src0 = peaks()
+        adv_gbs = BYTES_PER_UPDATE * M * NX * NY / (adv_ms * 1e-3) / 1e9
+        fo_line = {"value": fupd / (fms * 1e-3), "unit": "sample-cell-updates/s",
+                   "limiter": "FirstOrder (theta = 0)", "steps": args.steps,
+                   "ms_per_step": fms / args.steps, "advance_ms": adv_ms,
+                   "roofline": {"bound": "hbm", "kernel": "k_advance_tiled<1> (collide+stream)",
+                                "achieved": adv_gbs, "peak": hbm0, "unit": "GB/s",
+                                "frac": adv_gbs / hbm0, "peak_source": src0,
+                                "bytes_per_cell": BYTES_PER_UPDATE},
+                   "step_frac": BYTES_PER_UPDATE * fupd / (fms * 1e-3) / 1e9 / hbm0}
 
     # ---- post-processing (BASELINE configs[3]) ----
     post = None
@@ -538,8 +684,10 @@ def main():
                     "source": prof.get("source")}
             if ops:
                 rate = ops * cells_per_launch / t_tiles / 1e12
-                fp64.update({"achieved": rate, "peak": FP64_PEAK_TINST, "unit": "Tinst/s",
-                             "frac": rate / FP64_PEAK_TINST, "fp64_inst_per_cell": ops})
+                fpk, fsrc = fp64_peak()
+                fp64.update({"achieved": rate, "peak": fpk, "unit": "Tinst/s",
+                             "frac": rate / fpk, "peak_source": fsrc,
+                             "fp64_inst_per_cell": ops})
         line = {
             "metric": METRIC,
             "value": value, "unit": "sample-cell-updates/s", "n_gpus": ws,
@@ -561,7 +709,14 @@ def main():
             line["e2e"] = e2e
         if late:
             line["late_window"] = late
+        if fo_line:
+            line["first_order"] = fo_line
         if post:
+            if ws == 1 and not args.no_cpu_baseline:
+                try:
+                    post["cpu_baseline"] = postproc_cpu_baseline()
+                except Exception as exc:
+                    post["cpu_baseline"] = {"error": f"{type(exc).__name__}: {exc}"}
             line["postproc"] = post
         if not args.no_cpu_baseline and ws == 1:  # the reference CPU path: N = 1 only
             line["cpu_baseline"] = cpu_reference(args, ws)

@@ -153,6 +153,8 @@ class Oracle:
             self.f_fit = f("fit_rate", D, [I, DP, DP])
             self.f_march = f("march_timed", D, [G, Pp, Pe, U64, L, I, L, D, D, I, C.POINTER(L)])
             self.f_post = f("postproc_timed", D, [I, I, I, DP, DP, DP, DP])
+            self.f_window = f("march_window", D, [G, Pp, Pe, U64, L, I, D, L, D, I,
+                                                  C.POINTER(L), DP])
 
     def _check(self, rc):
         if rc != 0:
@@ -276,6 +278,25 @@ class Oracle:
         sec = self.f_march(C.byref(g), C.byref(p), C.byref(pp), base_seed, m0, n_samples, steps,
                            t_target, strip, threads, C.byref(upd))
         return sec, upd.value
+
+    def march_window(self, g, p, pp, base_seed, m0, n_samples, t_start, steps, strip=0.02,
+                     threads=1):
+        """Untimed run_sample loop to t_start, then `steps` timed steps of every
+        sample (reference only).  Returns (timed seconds, updates, pre seconds)."""
+        upd, pre = L(), D()
+        sec = self.f_window(C.byref(g), C.byref(p), C.byref(pp), base_seed, m0, n_samples,
+                            t_start, steps, strip, threads, C.byref(upd), C.byref(pre))
+        return sec, upd.value, pre.value
+
+    def postproc_timed(self, coarse, fine):
+        """restrict_field + wasserstein1 + strong_error as compute_metrics runs
+        them (single-threaded, reference only): (seconds, W1, E_strong)."""
+        coarse = np.ascontiguousarray(coarse, np.float64)
+        fine = np.ascontiguousarray(fine, np.float64)
+        M, _, nyc, nxc = coarse.shape
+        w1, es = D(), D()
+        sec = self.f_post(M, nxc, nyc, _dp(coarse), _dp(fine), C.byref(w1), C.byref(es))
+        return sec, w1.value, es.value
 
 
 @dataclass

@@ -429,6 +429,78 @@ double ref_march_timed(const vlbm_grid* gg, const vlbm_params* p, const vlbm_per
   return std::chrono::duration<double>(t1 - t0).count();
 }
 
+// The reference CPU march over a mid-run window, in two phases on `threads`
+// std::threads: (1, untimed) every sample is built as run_sample builds it
+// and marched with run_sample's loop body to t_start (dt clamped to hit it,
+// solver.hpp:645-657); (2, timed) each sample takes `steps` more iterations of
+// suggest_dt -> step -> state_finite (no clamp) -- the same trajectory the
+// GPU bench times after run_to(t_start).  Returns the wall seconds of phase
+// 2; the sample-cell updates of phase 2 go to *updates, phase 1's wall to
+// *pre_seconds.
+double ref_march_window(const vlbm_grid* gg, const vlbm_params* p, const vlbm_perturbation* pp,
+                        uint64_t base_seed, long m0, int n_samples, double t_start, long steps,
+                        double strip, int threads, long* updates, double* pre_seconds) {
+  const Grid grid = to_grid(gg);
+  const PerturbationParams pert = to_pert(pp);
+  const GasParams gas{p->gamma};
+  const LatticeParams lat = to_lattice(p);
+  std::vector<std::unique_ptr<Simulation>> sims(n_samples);
+  std::vector<char> alive(n_samples, 1);
+  const int nt = std::max(1, std::min(threads, n_samples));
+  auto pool_run = [&](auto&& body) {
+    std::atomic<int> next{0};
+    std::vector<std::thread> pool;
+    for (int w = 0; w < nt; ++w)
+      pool.emplace_back([&]() {
+        for (int t; (t = next.fetch_add(1)) < n_samples;) body(t);
+      });
+    for (auto& th : pool) th.join();
+  };
+  const auto t0 = std::chrono::steady_clock::now();
+  pool_run([&](int t) {
+    const ModeCoefficients coeffs = draw_coefficients(base_seed, m0 + t, pert.modes);
+    Boundaries bcs;
+    bcs.inlet_profile = [&pert, coeffs, gas](double y) { return inlet_state(y, coeffs, pert, gas); };
+    FieldSnapshot init = initial_field(grid, coeffs, pert, gas, strip);
+    sims[t] = std::make_unique<Simulation>(grid, lat, gas, std::move(bcs), init);
+    Simulation& sim = *sims[t];
+    sim.set_reference(pert.rho_amb, pert.p_amb);
+    constexpr double t_eps = 1e-12;  // solver.hpp:647
+    while (sim.time() < t_start - t_eps) {
+      double dt = sim.suggest_dt();
+      if (!std::isfinite(dt) || dt <= 0.0) {
+        alive[t] = 0;
+        return;
+      }
+      dt = std::min(dt, t_start - sim.time());
+      sim.step(dt);
+      if (!sim.state_finite()) {
+        alive[t] = 0;
+        return;
+      }
+    }
+  });
+  const auto t1 = std::chrono::steady_clock::now();
+  std::atomic<long> total{0};
+  pool_run([&](int t) {
+    if (!alive[t]) return;
+    Simulation& sim = *sims[t];
+    long done = 0;
+    for (long s = 0; s < steps; ++s) {
+      const double dt = sim.suggest_dt();
+      if (!std::isfinite(dt) || dt <= 0.0) break;
+      sim.step(dt);
+      ++done;
+      if (!sim.state_finite()) break;
+    }
+    total += done * static_cast<long>(grid.cells());
+  });
+  const auto t2 = std::chrono::steady_clock::now();
+  if (updates) *updates = total.load();
+  if (pre_seconds) *pre_seconds = std::chrono::duration<double>(t1 - t0).count();
+  return std::chrono::duration<double>(t2 - t1).count();
+}
+
 // wasserstein1 + strong_error (+ restrict_field of the fine ensemble) timed as
 // compute_metrics runs them (metrics.hpp:284-300), single-threaded.
 double ref_postproc_timed(int M, int nxc, int nyc, const double* coarse, const double* fine,

@@ -15,6 +15,7 @@
 #include <cstring>
 #include <limits>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "internal.h"
@@ -503,27 +504,56 @@ int vlbm_batch_create_coeffs(const vlbm_grid* g, const vlbm_params* p,
   q.p_ref = pp->p_amb;
   vlbm_batch* b = nullptr;
   if (int rc = alloc_batch(g, &q, n_samples, device, &b)) return rc;
+  // The inlet rows u_in(y_j) of every sample on the host (the reference's
+  // libm: perturbation.hpp:87-95), threads over samples; the initial field
+  // (ambient + the wedge of those rows) is then laid out on the device.
   const int K = pp->modes;
-  std::vector<double> rows(4 * (size_t)g->ny);
-  double* field = nullptr;
-  const size_t n = (size_t)g->nx * g->ny;
-  if (cudaMallocHost(&field, sizeof(double) * 4 * n) != cudaSuccess) {
+  const size_t nrow = 4 * (size_t)g->ny;
+  double* rows = nullptr;
+  if (cudaMallocHost(&rows, sizeof(double) * nrow * n_samples) != cudaSuccess) {
     free_batch(b);
     return set_error(VLBM_E_NOMEM, "pinned staging buffer");
   }
-  int rc = VLBM_OK;
-  for (int s = 0; s < n_samples && rc == VLBM_OK; ++s) {
-    const double* yc = y_all + (size_t)K * s;
-    const double* zc = z_all + (size_t)K * s;
-    for (int j = 0; j < g->ny; ++j)
-      vlbm_impl::inlet_state(vlbm_impl::y_center(*g, j), K, yc, zc, *pp, q.gamma,
-                             rows.data() + 4 * j);
-    vlbm_impl::initial_field(*g, K, yc, zc, *pp, q.gamma, strip_width, field);
-    rc = upload_sample(b, s, field, rows.data());
-    if (rc == VLBM_OK && cudaStreamSynchronize(b->stream) != cudaSuccess)
-      rc = set_error(VLBM_E_CUDA, "upload");
+  auto fill = [&](int s0, int s1) {
+    for (int s = s0; s < s1; ++s)
+      for (int j = 0; j < g->ny; ++j)
+        vlbm_impl::inlet_state(vlbm_impl::y_center(*g, j), K, y_all + (size_t)K * s,
+                               z_all + (size_t)K * s, *pp, q.gamma, rows + nrow * s + 4 * j);
+  };
+  const long long work = (long long)n_samples * g->ny;
+  int nt = work < 20000 ? 1
+                        : (int)std::min(std::max(1u, std::thread::hardware_concurrency()), 16u);
+  nt = std::min(nt, n_samples);
+  if (nt <= 1) {
+    fill(0, n_samples);
+  } else {
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t)
+      th.emplace_back(fill, (int)((long long)n_samples * t / nt),
+                      (int)((long long)n_samples * (t + 1) / nt));
+    for (auto& x : th) x.join();
   }
-  cudaFreeHost(field);
+  std::vector<int> counts(g->ny);
+  vlbm_impl::wedge_counts(*g, strip_width, counts.data());
+  const double amb[4] = {pp->rho_amb, 0.0, 0.0, pp->p_amb / (q.gamma - 1.0)};  // ambient_state
+  int* d_counts = nullptr;
+  int rc = VLBM_OK;
+  auto chk = [&](cudaError_t e, const char* what) {
+    if (e != cudaSuccess && rc == VLBM_OK)
+      rc = set_error(VLBM_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  };
+  chk(cudaMemcpyAsync(const_cast<double*>(b->P.inlet), rows, sizeof(double) * nrow * n_samples,
+                      cudaMemcpyHostToDevice, b->stream),
+      "upload inlet rows");
+  chk(cudaMalloc(&d_counts, sizeof(int) * g->ny), "malloc counts");
+  if (rc == VLBM_OK)
+    chk(cudaMemcpyAsync(d_counts, counts.data(), sizeof(int) * g->ny, cudaMemcpyHostToDevice,
+                        b->stream),
+        "upload counts");
+  if (rc == VLBM_OK) chk(vlbm_impl::launch_init_field(b->P, d_counts, amb, b->stream), "init field");
+  if (rc == VLBM_OK) chk(cudaStreamSynchronize(b->stream), "initial field");
+  cudaFree(d_counts);
+  cudaFreeHost(rows);
   if (rc == VLBM_OK) rc = finish_create(b);
   if (rc != VLBM_OK) {
     free_batch(b);

@@ -124,6 +124,20 @@ void initial_field(const vlbm_grid& g, int K, const double* yc, const double* zc
   }
 }
 
+// The wedge of initial_field row by row: counts[j] = the number of leading
+// cells with x_center(i) < w(y_j) (perturbation.hpp:116-119, the same
+// expressions), so the device can lay out ambient + wedge without libm.
+void wedge_counts(const vlbm_grid& g, double strip, int* counts) {
+  const double height = g.y_max - g.y_min;
+  for (int j = 0; j < g.ny; ++j) {
+    const double y = y_center(g, j);
+    const double w = strip * (0.5 + 5.0 * (y - g.y_min) / height);
+    int n = 0;
+    while (n < g.nx && x_center(g, n) < w) ++n;
+    counts[j] = n;
+  }
+}
+
 }  // namespace vlbm_impl
 
 extern "C" {

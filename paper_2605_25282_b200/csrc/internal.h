@@ -27,10 +27,16 @@ void inlet_state(double y, int K, const double* yc, const double* zc,
 // initial_field (perturbation.hpp:106-122) into 4 planes of ny x nx.
 void initial_field(const vlbm_grid& g, int K, const double* yc, const double* zc,
                    const vlbm_perturbation& pp, double gamma, double strip, double* out);
+// Leading wedge cells of initial_field per row (counts[ny]).
+void wedge_counts(const vlbm_grid& g, double strip, int* counts);
 
 // ---- march launchers (march.cu) -------------------------------------------
 cudaError_t launch_signal(const vlbm_dev::MarchParams& P, cudaStream_t st);
 cudaError_t launch_init(const vlbm_dev::MarchParams& P, double* d_a0, cudaStream_t st);
+// initial_field on the device from the uploaded inlet rows and wedge counts
+// (state buffer 0): ambient amb[4] except u_in(y_j) on cells i < counts[j].
+cudaError_t launch_init_field(const vlbm_dev::MarchParams& P, const int* counts,
+                              const double* amb4, cudaStream_t st);
 cudaError_t launch_sched(const vlbm_dev::MarchParams& P, double target, double fixed_dt,
                          cudaStream_t st);
 // part 0: the tile pass (u_FO, bounds, feasible(1), hard-cell queue);

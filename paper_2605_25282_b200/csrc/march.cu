@@ -74,6 +74,29 @@ __global__ void k_init_sched(MarchParams P, double* a0_out) {
   }
 }
 
+// initial_field (perturbation.hpp:106-122) laid out on the device: the
+// ambient state everywhere except the wedge cells i < counts[j] of row j,
+// which hold the inlet state u_in(y_j) -- the same row fill_ghosts uses for
+// the inlet ghosts, evaluated on the host with the reference's libm.  The
+// counts come from the host with the reference's comparison (wedge_counts).
+struct Amb4 {
+  double v[4];
+};
+__global__ void k_init_field(MarchParams P, const int* counts, Amb4 amb) {
+  const int s = blockIdx.y;
+  double* dst = P.buf0 + (long long)s * P.sample_stride;
+  const double* rows = P.inlet + (long long)s * P.ny * 4;
+  const long long n = (long long)P.nx * P.ny;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(idx / P.nx), i = (int)(idx - (long long)j * P.nx);
+    const bool wedge = i < counts[j];
+    const long long off = (long long)j * P.pitch + i;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) dst[k * P.plane + off] = wedge ? rows[4 * j + k] : amb.v[k];
+  }
+}
+
 // pops = M_k(u, a0) on the interior (solver.hpp:94-99).
 __global__ void k_init_pops(MarchParams P, const double* a0) {
   const int s = blockIdx.y;
@@ -363,6 +386,17 @@ cudaError_t launch_init(const MarchParams& P, double* d_a0, cudaStream_t st) {
   int bx = (int)((n + 255) / 256);
   if (bx > 1024) bx = 1024;
   k_init_pops<<<dim3(bx, P.S), 256, 0, st>>>(P, d_a0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init_field(const MarchParams& P, const int* counts, const double* amb4,
+                              cudaStream_t st) {
+  Amb4 amb;
+  for (int k = 0; k < 4; ++k) amb.v[k] = amb4[k];
+  const long long n = (long long)P.nx * P.ny;
+  int bx = (int)((n + 255) / 256);
+  if (bx > 1024) bx = 1024;
+  k_init_field<<<dim3(bx, P.S), 256, 0, st>>>(P, counts, amb);
   return cudaGetLastError();
 }
 

@@ -694,7 +694,8 @@ __global__ void __launch_bounds__(256, VLBM_UNC_MINB) k_bisect_unc(MarchParams P
       }
     }
     if (!P.replay) continue;
-    // stopped bisections -> the tail queue (bq storage; k_bisect_cert is done)
+    // stopped bisections -> the tail queue.  The tail has its own tq storage:
+    // k_bisect_cert may still be running on P.side, so bq must not be reused.
     int tbase, nt;
     const int t = warp_slot(stopped, P.hq_n + 7, &tbase, &nt);
     if (stopped) {
@@ -963,14 +964,18 @@ cudaError_t launch_theta_hard(const MarchParams& P, cudaStream_t st) {
       cs_ = P.side;
     }
     k_bisect_cert<<<148 * VLBM_CERT_GRID, 256, 0, cs_>>>(P);
-    if (P.side) {
-      if (cudaError_t e = cudaGetLastError()) return e;
-      if (cudaError_t e = cudaEventRecord(P.ev_join, P.side)) return e;
-    }
     k_bisect_unc<<<dim3(148 * VLBM_UNC_GRID, 3), 256, 0, st>>>(P);
     if (P.replay) k_bisect_tail<<<148 * VLBM_TAIL_GRID, 128, 0, st>>>(P);
-    if (P.side)
-      if (cudaError_t e = cudaStreamWaitEvent(st, P.ev_join, 0)) return e;
+    cudaError_t err = cudaGetLastError();
+    if (P.side) {
+      // once forked, always join (also on an error path): a stream left
+      // forked inside a graph capture would surface as an opaque
+      // "unjoined" capture failure instead of the real error
+      const cudaError_t ej = cudaEventRecord(P.ev_join, P.side);
+      const cudaError_t ew = cudaStreamWaitEvent(st, P.ev_join, 0);
+      if (err == cudaSuccess) err = ej != cudaSuccess ? ej : ew;
+    }
+    return err;
   }
   return cudaGetLastError();
 }

@@ -163,6 +163,10 @@ class PeerRows:
         if m_local:
             v._check(self.L.vlbm_ipc_handle(planes_local.data_ptr(), h, C.byref(off)))
         mine = (bytes(h), int(off.value), m_local, torch.cuda.current_device())
+        # the planes (often .contiguous() copies made just before, on this
+        # rank's stream) must be complete before any peer's kernel reads them:
+        # nothing else orders a peer's stream after ours (gloo does not)
+        torch.cuda.current_stream().synchronize()
         world = dist.get_world_size(group)
         allh = [None] * world
         dist.all_gather_object(allh, mine, group=group)

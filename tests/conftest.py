@@ -36,3 +36,17 @@ def vlbm():
     import paper_2605_25282_b200 as v
     v.lib()  # raises if the CUDA library is missing: no fallback
     return v
+
+
+@pytest.fixture(scope="session")
+def orc():
+    """The march oracle: oracle/_ref -- the unmodified reference compiled by
+    oracle/Makefile; its .so travels to the GPU box with the snapshot --
+    whenever it is built, else the pinned C restatement (oracle/vlbm_oracle.c).
+    Both expose the same calls (theta_cell / limiter_cells are restatement-only)."""
+    from oracle import oracle
+    if oracle.available("ref"):
+        return oracle.Oracle("ref")
+    if not oracle.available("vo"):
+        oracle.build(ref=False)
+    return oracle.Oracle("vo")

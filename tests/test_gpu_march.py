@@ -554,3 +554,23 @@ def test_cert_side_stream_matches_in_line(vlbm, vo, monkeypatch):
         r.step(min(r.suggest_dt(), 0.0008 - r.time))
     assert out["1"][1][1] == r.steps
     assert_bitwise(out["1"][0][1], r.get(), "side stream vs oracle")
+
+
+@pytest.mark.parametrize("nx,ny,strip", [(200, 40, 0.02), (37, 11, 0.3), (1000, 200, 0.02),
+                                         (64, 16, 0.0), (50, 10, 5.0)])
+def test_device_initial_field_bitwise(vlbm, orc, nx, ny, strip):
+    """The batch's initial field (inlet rows on the host, ambient + wedge laid
+    out on the device) and its equilibrium populations equal the reference's
+    initial_field + Simulation ctor (perturbation.hpp:106-122, solver.hpp:61-100)
+    bit for bit: thin, wide (strip 5: every row entirely wedge) and empty
+    (strip 0) wedges, ragged grids, several samples."""
+    x_max = 0.5 * nx / ny  # square cells (2.5 on the 5:1 jet grids)
+    g = vlbm.Grid(nx, ny, x_max)
+    S = 3
+    sim = vlbm.BatchSimulation.jet(g, n_samples=S, base_seed=42, m0=5, strip_width=strip)
+    for s in range(S):
+        r = orc.jet_sim(make_grid(nx, ny, x_max), make_params(), make_pert(), 42, 5 + s,
+                        strip=strip)
+        u, p = r.get(pops=True)
+        assert_bitwise(sim.state(s), u, f"initial u {nx}x{ny} strip {strip} sample {s}")
+        assert_bitwise(sim.populations(s), p, f"initial pops {nx}x{ny} strip {strip} sample {s}")
