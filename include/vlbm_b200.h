@@ -226,6 +226,15 @@ int vlbm_batch_kernel_ms(vlbm_batch* b, double* ms);
  * warps with vertex checks left, and three certificate statistics
  * (uncertified-but-feasible; of those with the true vertex minimum above
  * p_FO / 2; of those with the quadratic part dominant). */
+/* Limiter-queue statistics (cumulative since creation): out[0] queue
+ * capacity (entries, per sample group), out[1] sample groups (the queues
+ * are shared by groups marched one after another on the batch's stream when
+ * one set covering every cell of the batch does not fit in memory),
+ * out[2] cells finished in place because a queue was full (overflows; 0
+ * when the capacity covers a group's cells), out[3] the largest number of
+ * hard cells (theta = 1 infeasible) of one group in one step, out[4] hard
+ * cells summed over steps and groups, out[5] limiter passes counted. */
+int vlbm_batch_queue_stats(vlbm_batch* b, int64_t* out6);
 #define VLBM_AUDIT_COUNTERS 16
 int vlbm_batch_set_audit(vlbm_batch* b, int enable);
 int vlbm_batch_audit(vlbm_batch* b, int64_t* counters);

@@ -72,6 +72,10 @@ struct vlbm_batch {
   int* h_active_g = nullptr;     // pinned
   cudaEvent_t ev_fork = nullptr;
   bool cert_side = true;  // k_bisect_cert on a side stream (VLBM_CERT_SIDE=0: in line)
+  // serial sample groups: the groups share the batch's stream and ONE set of
+  // limiter queues (allocated by group 0), marched one after another
+  bool serial = false;
+  unsigned long long* d_qstats = nullptr;
   bool graphs = true;  // chunks after the first replay as a CUDA graph (VLBM_GRAPHS=0: off)
 };
 
@@ -101,13 +105,12 @@ void free_batch(vlbm_batch* b) {
   cudaFree(b->d_a0);
   for (size_t g = 0; g < b->Pg.size(); ++g) {
     MarchParams& Q = b->Pg[g];
+    if (b->serial && g > 0) continue;  // queues, side stream and events belong to group 0
     cudaFree(Q.hq);
     cudaFree(Q.hq_idx);
     cudaFree(Q.hq_n);
     cudaFree(Q.bq);
     cudaFree(Q.bq_idx);
-    cudaFree(Q.tq);
-    cudaFree(Q.tq_idx);
     if (Q.side) cudaStreamDestroy(Q.side);
     if (Q.ev_fork) cudaEventDestroy(Q.ev_fork);
     if (Q.ev_join) cudaEventDestroy(Q.ev_join);
@@ -116,6 +119,7 @@ void free_batch(vlbm_batch* b) {
     if (g > 0 && b->sg[g]) cudaStreamDestroy(b->sg[g]);
   }
   cudaFree(b->d_active_g);
+  cudaFree(b->d_qstats);
   if (b->h_active_g) cudaFreeHost(b->h_active_g);
   if (b->ev_fork) cudaEventDestroy(b->ev_fork);
   cudaFree(b->d_face_tx);
@@ -187,10 +191,8 @@ int alloc_batch(const vlbm_grid* g, const vlbm_params* p, int S, int device, vlb
   chk(cudaMalloc(&P.n_active, sizeof(int)), "malloc n_active");
   chk(cudaMalloc(&b->d_a0, sizeof(double) * S), "malloc a0");
   chk(cudaMallocHost(&b->h_active, sizeof(int)), "malloc host");
-  // Sample groups: the march runs G views of the batch (disjoint sample
-  // ranges: offset pointers, own control slice, limiter queues, tensor maps,
-  // counter and stream), so one group's HBM-bound advance overlaps another
-  // group's FP64-bound limiter.  VLBM_GROUPS overrides the default.
+  // Sample groups (below): the march runs G views of the batch (disjoint
+  // sample ranges: offset pointers, own control slice, tensor maps, counter).
   P.cert1 = 1;
   if (const char* e = getenv("VLBM_CERT1")) P.cert1 = atoi(e) != 0;
   P.replay = 1;
@@ -205,23 +207,46 @@ int alloc_batch(const vlbm_grid* g, const vlbm_params* p, int S, int device, vlb
       if (rc == VLBM_OK) chk(cudaMemset(P.cert_hint, 3, n), "memset cert_hint");
     }
   }
-  int G = 1;  // sample groups (VLBM_GROUPS): 2-4 measured 0.7-1.6% slower since the replay
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  if (const char* e = getenv("VLBM_GROUPS")) G = std::max(1, std::min(S, atoi(e)));
-  b->G = G;
   if (const char* e = getenv("VLBM_GRAPHS")) b->graphs = atoi(e) != 0;
   if (const char* e = getenv("VLBM_CERT_SIDE")) b->cert_side = atoi(e) != 0;
+  const bool rlmp = p->limiter == VLBM_LIMITER_RLMP;
+  // Limiter queues: per hard cell kHardWords (hq) + kBisWords (bq) +
+  // kUncWords (cq) doubles and three indices; the tail queue aliases hq.
+  const size_t entry =
+      sizeof(double) * (vlbm_dev::kHardWords + vlbm_dev::kBisWords + vlbm_dev::kUncWords) +
+      3 * sizeof(long long);
+  const size_t avail =
+      free_b > need + (size_t)(2ull << 30) ? free_b - need - (size_t)(2ull << 30) : 0;
+  const size_t qbudget = avail / 2;  // the other half stays free for the caller
+  const size_t cells_per_sample = (size_t)P.nx * P.ny;
+  // Sample groups.  Serial (the default when needed): when one set of queues
+  // covering every cell of the batch does not fit in qbudget, the batch is
+  // marched as G groups of samples, one after another on the batch's stream,
+  // sharing one set of queues that covers every cell of a group -- so no
+  // hard cell ever overflows (configs[2]: 125 samples of 4000x800).
+  // VLBM_SERIAL_GROUPS forces G (tests).  Concurrent (VLBM_GROUPS, an A/B
+  // switch: 2-4 groups measured 0.7-1.6 % slower since the replay): each
+  // group on its own stream with its own share of the queues.
+  int G = 1;
+  if (rlmp) {
+    if (const char* e = getenv("VLBM_SERIAL_GROUPS")) {
+      G = std::max(1, std::min(S, atoi(e)));
+    } else {
+      while (G < S && (size_t)((S + G - 1) / G) * cells_per_sample * entry > qbudget) ++G;
+    }
+    b->serial = G > 1;
+  }
+  if (!b->serial)
+    if (const char* e = getenv("VLBM_GROUPS")) G = std::max(1, std::min(S, atoi(e)));
+  b->G = G;
   chk(cudaMalloc(&b->d_active_g, sizeof(int) * G), "malloc active_g");
   chk(cudaMallocHost(&b->h_active_g, sizeof(int) * G), "malloc host active_g");
   chk(cudaEventCreateWithFlags(&b->ev_fork, cudaEventDisableTiming), "event");
-  // Limiter queues per group: up to every cell of the group, capped by memory
-  // (overflowing CTAs finish their hard cells in place).
-  const size_t entry =
-      sizeof(double) * (vlbm_dev::kHardWords + vlbm_dev::kBisWords + vlbm_dev::kUncWords) +
-      4 * sizeof(long long) + 2 * sizeof(double);
-  const size_t avail =
-      free_b > need + (size_t)(2ull << 30) ? free_b - need - (size_t)(2ull << 30) : 0;
+  chk(cudaMalloc(&b->d_qstats, 4 * sizeof(unsigned long long)), "malloc qstats");
+  if (rc == VLBM_OK) chk(cudaMemset(b->d_qstats, 0, 4 * sizeof(unsigned long long)), "memset");
+  P.qstats = b->d_qstats;
   for (int g = 0; g < G && rc == VLBM_OK; ++g) {
     const int s0 = (int)((long long)S * g / G), s1 = (int)((long long)S * (g + 1) / G);
     MarchParams Q = P;
@@ -234,12 +259,21 @@ int alloc_batch(const vlbm_grid* g, const vlbm_params* p, int S, int device, vlb
     Q.n_active = b->d_active_g + g;
     Q.cert_hint =
         P.cert_hint ? P.cert_hint + (size_t)s0 * vlbm_impl::theta_tiles(P.nx, P.ny) * 8 : nullptr;
-    Q.persist_ctas = std::max(1, sms * vlbm_impl::theta_ctas_per_sm() / G);
+    Q.persist_ctas = std::max(1, sms * vlbm_impl::theta_ctas_per_sm() / (b->serial ? 1 : G));
     cudaStream_t sg = b->stream;
-    if (g > 0) chk(cudaStreamCreateWithFlags(&sg, cudaStreamNonBlocking), "stream g");
-    if (p->limiter == VLBM_LIMITER_RLMP) {
-      size_t cap = (size_t)Q.S * P.nx * P.ny;
-      if (cap * entry > avail / 2 / G) cap = avail / 2 / G / entry;
+    if (g > 0 && !b->serial) chk(cudaStreamCreateWithFlags(&sg, cudaStreamNonBlocking), "stream g");
+    if (rlmp && b->serial && g > 0) {
+      const MarchParams& Q0 = b->Pg[0];  // the shared queues
+      Q.hq = Q0.hq, Q.hq_idx = Q0.hq_idx, Q.hq_n = Q0.hq_n, Q.hq_next = Q0.hq_next;
+      Q.hq_cap = Q0.hq_cap;
+      Q.bq = Q0.bq, Q.bq_idx = Q0.bq_idx, Q.tq = Q0.tq, Q.tq_idx = Q0.tq_idx;
+      Q.cq = Q0.cq, Q.cq_idx = Q0.cq_idx;
+      Q.side = Q0.side, Q.ev_fork = Q0.ev_fork, Q.ev_join = Q0.ev_join;
+    } else if (rlmp) {
+      const int Sg = b->serial ? (S + G - 1) / G : Q.S;
+      size_t cap = (size_t)Sg * cells_per_sample;
+      const size_t share = b->serial ? qbudget : qbudget / G;
+      if (cap * entry > share) cap = share / entry;
       if (cap > (size_t)INT_MAX / 2) cap = (size_t)INT_MAX / 2;
       if (const char* e = getenv("VLBM_HQ_CAP"))  // test hook: exercise the overflow paths
         cap = std::min(cap, (size_t)std::max(0ll, atoll(e)));
@@ -250,8 +284,8 @@ int alloc_batch(const vlbm_grid* g, const vlbm_params* p, int S, int device, vlb
         chk(cudaMalloc(&Q.hq_idx, sizeof(long long) * cap), "malloc hq_idx");
         chk(cudaMalloc(&Q.bq, sizeof(double) * vlbm_dev::kBisWords * cap), "malloc bq");
         chk(cudaMalloc(&Q.bq_idx, sizeof(long long) * cap), "malloc bq_idx");
-        chk(cudaMalloc(&Q.tq, sizeof(double) * 2 * cap), "malloc tq");
-        chk(cudaMalloc(&Q.tq_idx, sizeof(long long) * cap), "malloc tq_idx");
+        Q.tq = Q.hq;  // aliases: hq is dead once k_theta_hard has run
+        Q.tq_idx = Q.hq_idx;
         if (b->cert_side) {
           chk(cudaStreamCreateWithFlags(&Q.side, cudaStreamNonBlocking), "stream side");
           chk(cudaEventCreateWithFlags(&Q.ev_fork, cudaEventDisableTiming), "event");
@@ -259,7 +293,7 @@ int alloc_batch(const vlbm_grid* g, const vlbm_params* p, int S, int device, vlb
         }
         chk(cudaMalloc(&Q.cq, sizeof(double) * vlbm_dev::kUncWords * cap), "malloc cq");
         chk(cudaMalloc(&Q.cq_idx, sizeof(long long) * cap), "malloc cq_idx");
-        // counters: [0] hard cells, [2] bq, [3..5] cq bins, [6] limiter tile claims
+        // counters: [0] hard cells, [2] bq, [3..5] cq bins, [6] limiter tile claims, [7] tail
         chk(cudaMalloc(&Q.hq_n, 8 * sizeof(int)), "malloc hq_n");
         Q.hq_next = Q.hq_n + 1;
         if (rc == VLBM_OK) chk(cudaMemset(Q.hq_n, 0, 8 * sizeof(int)), "memset hq_n");
@@ -359,8 +393,10 @@ int march_loop(vlbm_batch* b, double target, double fixed_dt, int mode, int chun
   const int G = b->G;
   auto issue = [&](int n) -> int {
     // fork: the group streams start after everything queued on the main stream
-    if (G > 1) CU(cudaEventRecord(b->ev_fork, b->stream));
-    for (int g = 1; g < G; ++g) CU(cudaStreamWaitEvent(b->sg[g], b->ev_fork, 0));
+    if (G > 1 && !b->serial) {
+      CU(cudaEventRecord(b->ev_fork, b->stream));
+      for (int g = 1; g < G; ++g) CU(cudaStreamWaitEvent(b->sg[g], b->ev_fork, 0));
+    }
     for (int it = 0; it < n; ++it) {
       for (int g = 0; g < G; ++g) {  // groups interleaved: their kernels overlap
         const MarchParams& Q = b->Pg[g];
@@ -389,7 +425,7 @@ int march_loop(vlbm_batch* b, double target, double fixed_dt, int mode, int chun
   // the call, the per-step state lives on the device). Not while per-launch
   // timing is on (its events are harvested on the host) or with several
   // sample groups.
-  const bool use_graph = b->graphs && !b->timing && G == 1;
+  const bool use_graph = b->graphs && !b->timing && (G == 1 || b->serial);
   cudaGraphExec_t exec = nullptr;
   int exec_chunk = -1;
   long long exec_launches = 0;
@@ -437,7 +473,8 @@ int march_loop(vlbm_batch* b, double target, double fixed_dt, int mode, int chun
     for (int g = 0; g < G && e == cudaSuccess; ++g)
       e = cudaMemcpyAsync(b->h_active_g + g, b->Pg[g].n_active, sizeof(int),
                           cudaMemcpyDeviceToHost, b->sg[g]);
-    for (int g = 0; g < G && e == cudaSuccess; ++g) e = cudaStreamSynchronize(b->sg[g]);
+    for (int g = 0; g < G && e == cudaSuccess; ++g)
+      if (g == 0 || !b->serial) e = cudaStreamSynchronize(b->sg[g]);
     if (e != cudaSuccess) {
       rc = set_error(VLBM_E_CUDA, std::string("march poll: ") + cudaGetErrorString(e));
       break;
@@ -761,6 +798,18 @@ int vlbm_batch_audit(vlbm_batch* b, int64_t* counters) {
     CU(cudaStreamSynchronize(b->stream));
   }
   for (int k = 0; k < VLBM_AUDIT_COUNTERS; ++k) counters[k] = h[k];
+  return VLBM_OK;
+}
+
+int vlbm_batch_queue_stats(vlbm_batch* b, int64_t* out) {
+  if (!b || !out) return set_error(VLBM_E_INVALID, "null argument");
+  CU(cudaSetDevice(b->device));
+  unsigned long long h[4] = {0, 0, 0, 0};
+  CU(cudaMemcpyAsync(h, b->d_qstats, sizeof(h), cudaMemcpyDeviceToHost, b->stream));
+  CU(cudaStreamSynchronize(b->stream));
+  out[0] = b->Pg.empty() ? 0 : b->Pg[0].hq_cap;
+  out[1] = b->G;
+  for (int k = 0; k < 4; ++k) out[2 + k] = (int64_t)h[k];
   return VLBM_OK;
 }
 

@@ -169,8 +169,15 @@ __global__ void k_sched(MarchParams P, double target, double fixed_dt) {
   __syncthreads();
   if (threadIdx.x == 0) {
     *P.n_active = s_count;
-    if (P.hq_n)  // empty the limiter queues
+    if (P.hq_n) {  // record the last pass's hard cells, then empty the queues
+      const unsigned long long h = (unsigned long long)P.hq_n[0];
+      if (P.qstats && P.hq_n[6] > 0) {  // a tile pass ran since the last reset
+        if (h > P.qstats[1]) P.qstats[1] = h;
+        P.qstats[2] += h;
+        P.qstats[3] += 1;
+      }
       for (int k = 0; k < 8; ++k) P.hq_n[k] = 0;
+    }
   }
 }
 

@@ -69,14 +69,20 @@ struct MarchParams {
   //   *_idx: cell index; cq_idx packs the uncertified-vertex mask in bits 40..55
   double* bq;
   long long* bq_idx;
-  // Tail queue of k_bisect_unc (its own storage, so k_bisect_cert can run
-  // beside it): lo, hi (2 x hq_cap doubles); tq_idx = cq slot | step << 40.
+  // Tail queue of k_bisect_unc: lo, hi (2 x hq_cap doubles); tq_idx = cq
+  // slot | step << 40.  It aliases the first two word planes of hq and hq_idx
+  // (dead once k_theta_hard has run; k_bisect_cert, which may run beside
+  // k_bisect_unc on `side`, reads only bq).
   double* tq;
   long long* tq_idx;
   cudaStream_t side;               // k_bisect_cert's stream (joined before the advance)
   cudaEvent_t ev_fork, ev_join;    // fork after k_theta_hard / join after k_bisect_cert
   double* cq;
   long long* cq_idx;
+  // Queue statistics (cumulative, never reset): [0] cells finished in place
+  // because a queue was full, [1] peak hard cells of one pass, [2] hard cells
+  // summed over passes, [3] passes.  Updated by the limiter kernels / k_sched.
+  unsigned long long* qstats;
   int* audit;    // optional: disagreements of the certified bisection (must stay 0)
   int cert1;     // use the theta = 1 vertex certificate (A/B switch VLBM_CERT1, default on)
   int replay;    // k_bisect_unc replays its bisections from certified classifications
@@ -90,6 +96,7 @@ struct MarchParams {
   // TMA tensor maps [x, y, plane, sample] of buffer 0/1 with the tile boxes of
   // the advance (34x10x20), the limiter's u (36x12x4) and populations (34x10x16).
   CUtensorMap tm_adv[2], tm_thu[2], tm_thp[2];
+  CUtensorMap tm_adv2[2];  // k_advance_v2's u box (68x10x4)
   double dx, gamma, gm1, alpha, w, safety, kappa, rho_floor_coef, p_floor_coef;
   double rho_ref, p_ref;
   int bc[4];

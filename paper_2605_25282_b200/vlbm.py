@@ -186,6 +186,7 @@ def lib() -> C.CDLL:
     sig("vlbm_batch_kernel_ms", I, [V, DP])
     sig("vlbm_batch_set_audit", I, [V, I])
     sig("vlbm_batch_audit", I, [V, C.POINTER(I64)])
+    sig("vlbm_batch_queue_stats", I, [V, C.POINTER(I64)])
     sig("vlbm_restrict_field", I, [I, I, DP, DP])
     sig("vlbm_strong_error", I, [I, I64, DP, DP, DP, DP])
     sig("vlbm_wasserstein1", I, [I, I64, DP, DP, I, DP])
@@ -389,6 +390,14 @@ class BatchSimulation:
         return dict(launches=la.value, ms_theta=mt.value, ms_advance=ma.value,
                     ms_sched=ms.value, cell_updates=cu.value, ms_theta_tiles=km[0],
                     ms_theta_hard=km[1])
+
+    def queue_stats(self) -> dict:
+        """Limiter-queue capacity, sample groups and overflow / hard-cell
+        counters (cumulative since creation; vlbm_batch_queue_stats)."""
+        n = (I64 * 6)()
+        _check(lib().vlbm_batch_queue_stats(self._h, n))
+        return dict(capacity=n[0], groups=n[1], overflow=n[2], peak_hard=n[3],
+                    hard_total=n[4], passes=n[5])
 
     def set_audit(self, on: bool = True) -> None:
         """Re-check every certified bisection step with the full feasible()."""

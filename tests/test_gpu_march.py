@@ -330,6 +330,38 @@ def test_limiter_queue_overflow_paths_bitwise(vlbm, vo, monkeypatch, cap):
             r.step(min(r.suggest_dt(), 0.0008 - r.time))
         assert steps[m] == r.steps
         assert_bitwise(sim.state(m), r.get(), f"overflow cap {cap} sample {m}")
+    q = sim.queue_stats()
+    if cap != "0":  # the overflow counter sees the cells finished in place
+        assert q["capacity"] == int(cap) and q["overflow"] > 0 and q["peak_hard"] > int(cap)
+
+
+@pytest.mark.parametrize("groups,cap", [(3, None), (8, None), (3, "1536")])
+def test_serial_sample_groups_bitwise(vlbm, orc, monkeypatch, groups, cap):
+    """Serial sample groups (the configs[2] layout: groups of samples marched
+    one after another on one stream, sharing one set of limiter queues that
+    covers every cell of a group): fields, times and step counts
+    bit-identical to the reference at late time; no overflow when the queue
+    covers a group (the overflow counter counts the cells finished in place
+    when it does not)."""
+    monkeypatch.setenv("VLBM_SERIAL_GROUPS", str(groups))
+    if cap:
+        monkeypatch.setenv("VLBM_HQ_CAP", cap)
+    g = vlbm.Grid(200, 40)
+    sim = vlbm.BatchSimulation.jet(g, n_samples=8, base_seed=42)
+    sim.run_to(0.0008)
+    t, steps, status = sim.scalars()
+    q = sim.queue_stats()
+    assert q["groups"] == groups and q["passes"] > 0 and q["peak_hard"] > 0
+    if cap:
+        assert q["overflow"] > 0
+    else:
+        assert q["overflow"] == 0 and q["capacity"] >= 8 // groups * 8000
+    for m in (0, 4, 7):
+        r = orc.jet_sim(make_grid(200, 40), make_params(), make_pert(), 42, m)
+        while r.time < 0.0008 - 1e-12:
+            r.step(min(r.suggest_dt(), 0.0008 - r.time))
+        assert steps[m] == r.steps and bits(t[m]) == bits(r.time)
+        assert_bitwise(sim.state(m), r.get(), f"serial groups {groups} sample {m}")
 
 
 @pytest.mark.parametrize("limiter", [RLMP, FIRST_ORDER])
