@@ -29,6 +29,8 @@
  *   vlbm_ensemble_moments    ensemble_moments               metrics.hpp:148-177
  *   vlbm_d_w1_restrict_mean  wasserstein1 on device planes  metrics.hpp:97-125
  *                            (restriction fused, storage-order mean overlapped)
+ *   vlbm_metrics_*           compute_metrics' per (pair, time) W1 + E_strong
+ *                            with one upload per ensemble   metrics.hpp:259-327
  *   vlbm_d_w1_rows           wasserstein1's per-cell terms over samples held on
  *                            several GPUs (row tables, CUDA-IPC peer mappings):
  *                            compute_metrics' W1 across a sample-sharded node
@@ -271,6 +273,22 @@ int vlbm_d_strong_partials_var(int M, int nxc, int nyc, const double* d_coarse, 
 /* strong_error's host tail (metrics.hpp:81-89) over M x 10 partials (host
  * copy): throws-equivalent VLBM_E_DOMAIN on a zero reference norm. */
 int vlbm_strong_finish(int M, const double* partials, double* result, double* per_component);
+
+/* compute_metrics' reductions for one (grid pair, snapshot time) with each
+ * ensemble uploaded once (metrics.hpp:284-300): begin with the number of
+ * jointly valid samples M (M* of the pair), the coarse grid and the metric
+ * variable; add the samples in order, in any batches (host fields: coarse
+ * [count][4][nyc][nxc], fine [count][4][2nyc][2nxc]) -- each batch's
+ * strong_error partials are taken on the device at once and the metric
+ * variable's planes kept there; finish runs wasserstein1 (restriction fused)
+ * and the strong_error tail.  Results bit-identical to wasserstein1 and
+ * strong_error on the restricted fields. */
+typedef struct vlbm_metrics vlbm_metrics;
+int vlbm_metrics_begin(int M, int nxc, int nyc, int var, int device, vlbm_metrics** out);
+int vlbm_metrics_add(vlbm_metrics* m, int first, int count, const double* coarse,
+                     const double* fine);
+int vlbm_metrics_finish(vlbm_metrics* m, double* w1, double* e_strong, double* per_component);
+void vlbm_metrics_destroy(vlbm_metrics* m);
 /* W1 per-cell terms of coarse planes vs the on-the-fly restriction of fine
  * planes (one variable, addressing as vlbm_d_strong_partials_var). */
 int vlbm_d_w1_restrict(int M, int nxc, int nyc, const double* d_coarse, int64_t c_stride,

@@ -20,6 +20,7 @@
 
 #include <cmath>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <exception>
 #include <mutex>
@@ -410,8 +411,14 @@ inline std::pair<FieldSnapshot, FieldSnapshot> ensemble_moments(
 
 // compute_metrics (metrics.hpp:259-327): W1, E_strong and M* per grid pair and
 // snapshot time, then the per-time rate fits (host scalar work, reference
-// fit_rate), with the per-pair reductions on the device.
-inline MetricsReport compute_metrics(const EnsembleManifest& man) {
+// fit_rate).  Device resident: for each (pair, time) the jointly valid
+// samples' coarse and fine snapshots are read (reference read_snapshot) in
+// batches on a reader thread while the device takes the previous batch --
+// each ensemble is uploaded once (vlbm_metrics_*: strong_error partials with
+// the restriction fused as each batch lands, the metric variable's planes
+// kept on the device, W1 over them at the end); no field is restricted or
+// reduced on the host.
+inline MetricsReport compute_metrics(const EnsembleManifest& man, int device = 0) {
   const CaseConfig& cfg = man.config;
   if (cfg.grids.size() < 2) throw std::runtime_error("metrics: need >= 2 grids for Cauchy errors");
   const Variable var = variable_from_name(cfg.metric_variable);
@@ -428,23 +435,58 @@ inline MetricsReport compute_metrics(const EnsembleManifest& man) {
     const ValidityMask mask = joint_validity(man, p, p + 1);
     const int m_star = mask.m_star();
     if (m_star < 1) throw std::runtime_error("metrics: no jointly valid samples for pair");
+    std::vector<std::size_t> valid;
+    for (std::size_t m = 0; m < man.samples.size(); ++m)
+      if (mask.mask[m]) valid.push_back(m);
+    const std::size_t nc = static_cast<std::size_t>(cg.cells()), nf = 4 * nc;
+    // reader batches of about 256 MiB of host fields
+    const std::size_t B = std::max<std::size_t>(
+        1, std::min<std::size_t>(valid.size(), (256u << 20) / (32 * (nc + nf))));
     for (std::size_t ti = 0; ti < n_times; ++ti) {
-      std::vector<FieldSnapshot> coarse, restricted;
-      for (std::size_t m = 0; m < man.samples.size(); ++m) {
-        if (!mask.mask[m]) continue;
-        coarse.push_back(read_snapshot(man.root / man.samples[m].files[p][ti], cg));
-        restricted.push_back(
-            gpu::restrict_field(read_snapshot(man.root / man.samples[m].files[p + 1][ti], fg)));
+      struct Batch {
+        std::vector<double> c, f;
+      };
+      auto read_batch = [&](std::size_t b0, Batch& out) {
+        const std::size_t nb = std::min(B, valid.size() - b0);
+        out.c.resize(4 * nc * nb);
+        out.f.resize(4 * nf * nb);
+        for (std::size_t k = 0; k < nb; ++k) {
+          const auto& rec = man.samples[valid[b0 + k]];
+          to_planes(read_snapshot(man.root / rec.files[p][ti], cg), &out.c[4 * nc * k]);
+          to_planes(read_snapshot(man.root / rec.files[p + 1][ti], fg), &out.f[4 * nf * k]);
+        }
+      };
+      vlbm_metrics* ctx = nullptr;
+      check(vlbm_metrics_begin(m_star, cg.nx, cg.ny, static_cast<int>(var), device, &ctx));
+      struct Guard {
+        vlbm_metrics* c;
+        ~Guard() { vlbm_metrics_destroy(c); }
+      } guard{ctx};
+      Batch cur, next;
+      read_batch(0, cur);
+      for (std::size_t b0 = 0; b0 < valid.size(); b0 += B) {
+        std::exception_ptr err;
+        std::thread reader;
+        if (b0 + B < valid.size())
+          reader = std::thread([&] {
+            try {
+              read_batch(b0 + B, next);
+            } catch (...) {
+              err = std::current_exception();
+            }
+          });
+        const int nb = static_cast<int>(std::min(B, valid.size() - b0));
+        const int rc = vlbm_metrics_add(ctx, static_cast<int>(b0), nb, cur.c.data(), cur.f.data());
+        if (reader.joinable()) reader.join();
+        check(rc);
+        if (err) std::rethrow_exception(err);
+        std::swap(cur, next);
       }
-      std::vector<const FieldSnapshot*> ca, cb;
-      for (const auto& s : coarse) ca.push_back(&s);
-      for (const auto& s : restricted) cb.push_back(&s);
       MetricsRow row;
       row.time = cfg.snapshot_times[ti];
       row.pair = std::to_string(cg.nx) + "->" + std::to_string(fg.nx);
       row.m_star = m_star;
-      row.w1 = gpu::wasserstein1(ca, cb, var);
-      row.e_strong = gpu::strong_error(coarse, restricted);
+      check(vlbm_metrics_finish(ctx, &row.w1, &row.e_strong, nullptr));
       w1s[p][ti] = row.w1;
       strongs[p][ti] = row.e_strong;
       rep.rows.push_back(row);

@@ -30,7 +30,7 @@ NVCC_FLAGS = ARCH + [
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math", "-I", INCLUDE,
              "-I", "/usr/local/cuda/include"]
 
-CU_SOURCES = ["march.cu", "march_tiled.cu", "post.cu", "capi.cu"]
+CU_SOURCES = ["march.cu", "march_tiled.cu", "post.cu", "capi.cu", "metrics_ctx.cu"]
 CPP_SOURCES = ["host_ic.cpp"]
 HEADERS = ["vlbm_device.cuh", "march.cuh", "march_common.cuh", "rlmp.cuh", "rlmp_replay.cuh", "internal.h"]
 

@@ -277,7 +277,9 @@ int alloc_batch(const vlbm_grid* g, const vlbm_params* p, int S, int device, vlb
       if (cap > (size_t)INT_MAX / 2) cap = (size_t)INT_MAX / 2;
       if (const char* e = getenv("VLBM_HQ_CAP"))  // test hook: exercise the overflow paths
         cap = std::min(cap, (size_t)std::max(0ll, atoll(e)));
-      cap = cap / 768 * 768;  // even thirds of whole kHB chunks: 16-B aligned bulk copies
+      // even thirds of whole kHB chunks (16-B aligned bulk copies): rounded up
+      // when memory allows, so a queue meant to cover a group's cells does
+      cap = (cap + 767) / 768 * 768 * entry <= share ? (cap + 767) / 768 * 768 : cap / 768 * 768;
       if (cap >= 1024) {
         Q.hq_cap = (int)cap;
         chk(cudaMalloc(&Q.hq, sizeof(double) * vlbm_dev::kHardWords * cap), "malloc hq");
@@ -780,8 +782,8 @@ int vlbm_batch_set_audit(vlbm_batch* b, int enable) {
   if (!b) return set_error(VLBM_E_INVALID, "null batch");
   CU(cudaSetDevice(b->device));
   if (enable && !b->P.audit) {
-    CU(cudaMalloc(&b->P.audit, VLBM_AUDIT_COUNTERS * sizeof(int)));
-    CU(cudaMemset(b->P.audit, 0, VLBM_AUDIT_COUNTERS * sizeof(int)));
+    CU(cudaMalloc(&b->P.audit, VLBM_AUDIT_COUNTERS * sizeof(vlbm_dev::AuditCtr)));
+    CU(cudaMemset(b->P.audit, 0, VLBM_AUDIT_COUNTERS * sizeof(vlbm_dev::AuditCtr)));
   } else if (!enable && b->P.audit) {
     CU(cudaFree(b->P.audit));
     b->P.audit = nullptr;
@@ -792,12 +794,12 @@ int vlbm_batch_set_audit(vlbm_batch* b, int enable) {
 
 int vlbm_batch_audit(vlbm_batch* b, int64_t* counters) {
   if (!b || !counters) return set_error(VLBM_E_INVALID, "null argument");
-  int h[VLBM_AUDIT_COUNTERS] = {};
+  vlbm_dev::AuditCtr h[VLBM_AUDIT_COUNTERS] = {};
   if (b->P.audit) {
     CU(cudaMemcpyAsync(h, b->P.audit, sizeof(h), cudaMemcpyDeviceToHost, b->stream));
     CU(cudaStreamSynchronize(b->stream));
   }
-  for (int k = 0; k < VLBM_AUDIT_COUNTERS; ++k) counters[k] = h[k];
+  for (int k = 0; k < VLBM_AUDIT_COUNTERS; ++k) counters[k] = (int64_t)h[k];
   return VLBM_OK;
 }
 

@@ -83,7 +83,7 @@ struct MarchParams {
   // because a queue was full, [1] peak hard cells of one pass, [2] hard cells
   // summed over passes, [3] passes.  Updated by the limiter kernels / k_sched.
   unsigned long long* qstats;
-  int* audit;    // optional: disagreements of the certified bisection (must stay 0)
+  AuditCtr* audit;    // optional: disagreements of the certified bisection (must stay 0)
   int cert1;     // use the theta = 1 vertex certificate (A/B switch VLBM_CERT1, default on)
   int replay;    // k_bisect_unc replays its bisections from certified classifications
                  // (rlmp_replay.cuh; A/B switch VLBM_REPLAY, default on)
@@ -96,7 +96,6 @@ struct MarchParams {
   // TMA tensor maps [x, y, plane, sample] of buffer 0/1 with the tile boxes of
   // the advance (34x10x20), the limiter's u (36x12x4) and populations (34x10x16).
   CUtensorMap tm_adv[2], tm_thu[2], tm_thp[2];
-  CUtensorMap tm_adv2[2];  // k_advance_v2's u box (68x10x4)
   double dx, gamma, gm1, alpha, w, safety, kappa, rho_floor_coef, p_floor_coef;
   double rho_ref, p_ref;
   int bc[4];

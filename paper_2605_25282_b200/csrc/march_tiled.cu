@@ -68,11 +68,6 @@ constexpr unsigned kThetaTx = sizeof(double) * (4 * NR2 + kThetaSPn);
 constexpr int kAdvF = 4 * NA;
 constexpr size_t kAdvanceSmem = sizeof(double) * (kAdvF + 8 * NA);
 constexpr unsigned kAdvanceTx = sizeof(double) * 4 * NA;
-// k_advance_v2: 64 x 8 tiles, two x-adjacent cells per thread (128-bit
-// accesses); staged u box 68 x 10 (x from x0 - 2: even, 16-B aligned).
-constexpr int TX2 = 64, AX2 = TX2 + 4, NA2 = AX2 * AY;  // 68 x 10
-constexpr size_t kAdv2Smem = sizeof(double) * 12 * NA2;  // u [4][NA2] | F [8][NA2]
-constexpr unsigned kAdv2Tx = sizeof(double) * 4 * NA2;
 }  // namespace tiled
 
 // ---- TMA + mbarrier (PTX) -----------------------------------------------------
@@ -422,6 +417,7 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_THETA_MINB)
         P.cert_hint ? P.cert_hint + (long long)t * 8 + (threadIdx.x >> 5) : nullptr;
     const int h0 = hint ? *hint : 3;
     const bool try_cert = P.cert1 && (h0 >= VLBM_CERT_TRY || (c->steps % kCertProbe) == 0);
+    unsigned aflags = 0;  // audit statistics of this cell (bits = counter indices)
     if (valid) {
       if (diag_ok(1.0, foC, delta, b, gm1)) {
         double parts[2] = {0.0, 0.0};
@@ -431,10 +427,10 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_THETA_MINB)
         need = !cert;
         const bool ok = cert || vertex_floors_ok(1.0, foC, cf, b, gm1);
         if (P.audit) {  // [8] diagonal passed, [9] certified, [10] feasible; [0] certificate errors
-          atomicAdd(P.audit + 8, 1);
-          if (cert) atomicAdd(P.audit + 9, 1);
-          if (ok) atomicAdd(P.audit + 10, 1);
-          if (cert && !vertex_floors_ok(1.0, foC, cf, b, gm1)) atomicAdd(P.audit, 1);
+          aflags |= 1u << 8;
+          if (cert) aflags |= 1u << 9;
+          if (ok) aflags |= 1u << 10;
+          if (cert && !vertex_floors_ok(1.0, foC, cf, b, gm1)) aflags |= 1u;
           if (!cert && ok) {
             // [12] uncertified but feasible; [13] of those the true vertex
             // minimum is above p_FO / 2 (bound loose); [14] quadratic part
@@ -442,9 +438,9 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_THETA_MINB)
             double pmin = pfo0;
             for (int mask = 1; mask < 16; ++mask)
               pmin = smin(pmin, pressure(vertex_at(foC, cf, mask), gm1));
-            atomicAdd(P.audit + 12, 1);
-            if (pmin > 0.5 * pfo0) atomicAdd(P.audit + 13, 1);
-            if (parts[1] > parts[0]) atomicAdd(P.audit + 14, 1);
+            aflags |= 1u << 12;
+            if (pmin > 0.5 * pfo0) aflags |= 1u << 13;
+            if (parts[1] > parts[0]) aflags |= 1u << 14;
           }
         }
         if (ok)
@@ -459,7 +455,13 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_THETA_MINB)
       const unsigned m = __ballot_sync(0xffffffffu, need);
       if ((threadIdx.x & 31) == 0) {
         if (hint && try_cert) *hint = (unsigned char)(m == 0 ? min(h0 + 1, 3) : max(h0 - 1, 0));
-        if (P.audit && m) atomicAdd(P.audit + 11, 1);  // [11] warps with vertex checks left
+        if (P.audit && m) atomicAdd(P.audit + 11, 1ull);  // [11] warps with vertex checks left
+      }
+      if (P.audit) {  // warp-aggregated: one atomic per counter and warp
+        for (int k = 0; k < 15; ++k) {
+          const unsigned mk = __ballot_sync(0xffffffffu, (aflags >> k) & 1u);
+          if ((threadIdx.x & 31) == 0 && mk) atomicAdd(P.audit + k, (AuditCtr)__popc(mk));
+        }
       }
     }
     const long long cell = (long long)s * P.plane + (long long)j * P.pitch + i;
@@ -560,8 +562,8 @@ __global__ void __launch_bounds__(256, 2) k_theta_hard(MarchParams P) {
           P.theta[idx] = h.result;
         } else {
           if (P.audit) {
-            atomicAdd(P.audit + 1, 1);
-            atomicAdd(P.audit + (h.unc ? 3 : 2), 1);
+            atomicAdd(P.audit + 1, 1ull);
+            atomicAdd(P.audit + (h.unc ? 3 : 2), 1ull);
           }
           cls = (h.unc || P.audit) ? 2 : 1;
           ccls = unc_class(h.unc);
@@ -850,237 +852,6 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_ADV_MINB)
   reduce_signal(c, bits, bad, nonfin);
 }
 
-// ---------------------------------------------------------------------------
-// k_advance_v2 -- the blended pull stream-collide (solver.hpp:536-575) with
-// 128-bit accesses: a CTA owns a 64 x 8 tile, each thread the two x-adjacent
-// cells (i0, i0 + 1), i0 = x0 + 2 * lane, of row y0 + warp.  On interior
-// tiles (every cell's four neighbours inside the domain) every state plane
-// is read and written as double2 pairs, coalesced 512 B per warp and
-// instruction: the thread's own 16 population pairs, the south / north
-// pulls (pop 2 of row j-1, pop 3 of row j+1: pairs), and the x pulls come
-// from the lane neighbours' own pairs by shuffles (pop 0 of i0 - 1 is the
-// previous lane's second cell, pop 1 of i0 + 2 the next lane's first; lanes
-// 0 / 31 load that one value).  Cell theta and its face minima the same
-// way.  u arrives by TMA on the 68 x 10 box and the Maxwellians of the
-// staged cells are formed from inv2a*f, inv2a*g exactly as in
-// k_advance_tiled; the populations are processed one direction at a time so
-// the pairs do not all live at once.  Boundary tiles run the per-cell form
-// (fill_ghosts values, generic face thetas) for both cells.  Every
-// expression keeps the reference's operation order: bit-identical results.
-__device__ __forceinline__ double2 ld2(const double* p) {
-  return *reinterpret_cast<const double2*>(p);
-}
-__device__ __forceinline__ void st2cs(double* p, double a, double b) {
-#if VLBM_STORE_CS
-  __stcs(reinterpret_cast<double2*>(p), make_double2(a, b));
-#else
-  *reinterpret_cast<double2*>(p) = make_double2(a, b);
-#endif
-}
-// planes c = 0..3 of a 4-plane group at offset off, cells off and off + 1
-struct cs2 {
-  cs a, b;
-};
-__device__ __forceinline__ cs2 ld_pair4(const double* base, long long plane, long long off) {
-  const double2 r = ld2(base + off), mx = ld2(base + plane + off), my = ld2(base + 2 * plane + off),
-                e = ld2(base + 3 * plane + off);
-  return {{r.x, mx.x, my.x, e.x}, {r.y, mx.y, my.y, e.y}};
-}
-__device__ __forceinline__ void st_pair4(double* base, long long plane, long long off, const cs& a,
-                                         const cs& b) {
-  st2cs(base + off, a.r, b.r);
-  st2cs(base + plane + off, a.mx, b.mx);
-  st2cs(base + 2 * plane + off, a.my, b.my);
-  st2cs(base + 3 * plane + off, a.e, b.e);
-}
-__device__ __forceinline__ cs shfl_up4(const cs& v, unsigned d) {
-  return {__shfl_up_sync(0xffffffffu, v.r, d), __shfl_up_sync(0xffffffffu, v.mx, d),
-          __shfl_up_sync(0xffffffffu, v.my, d), __shfl_up_sync(0xffffffffu, v.e, d)};
-}
-__device__ __forceinline__ cs shfl_down4(const cs& v, unsigned d) {
-  return {__shfl_down_sync(0xffffffffu, v.r, d), __shfl_down_sync(0xffffffffu, v.mx, d),
-          __shfl_down_sync(0xffffffffu, v.my, d), __shfl_down_sync(0xffffffffu, v.e, d)};
-}
-// staged M_k of the cell pair (q, q + 1), q even: 128-bit shared loads
-__device__ __forceinline__ cs2 staged_m2(const double* U, const double* F, int q, int k,
-                                         double w) {
-  constexpr int N = tiled::NA2;
-  const double* Fk = F + (k < 2 ? 0 : 4 * N);
-  cs2 r;
-  double* ra = &r.a.r;
-  double* rb = &r.b.r;
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    const double2 u = ld2(U + c * N + q), f = ld2(Fk + c * N + q);
-    const double wa = w * u.x, wb = w * u.y;
-    ra[c] = (k & 1) ? wa - f.x : wa + f.x;
-    rb[c] = (k & 1) ? wb - f.y : wb + f.y;
-  }
-  return r;
-}
-
-#ifndef VLBM_ADV2_MINB
-#define VLBM_ADV2_MINB 2
-#endif
-template <int kMode>
-__global__ void __launch_bounds__(tiled::NT, VLBM_ADV2_MINB)
-    k_advance_v2(MarchParams P, double const_theta, const __grid_constant__ CUtensorMap tma0,
-                 const __grid_constant__ CUtensorMap tma1) {
-  using namespace tiled;
-  extern __shared__ __align__(128) double sm[];
-  __shared__ __align__(8) unsigned long long bar;
-  const int s = blockIdx.z;
-  SampleCtl* c = P.ctl + s;
-  if (!c->active) return;
-  double* R = sm;             // [4][NA2]: u (TMA)
-  double* F = sm + 4 * NA2;   // [8][NA2]: inv2a f, inv2a g
-  const int x0 = blockIdx.x * TX2, y0 = blockIdx.y * TY;
-  const int parity = c->parity;
-  const double* src = state_src(P, s, parity);
-  double* dst = state_dst(P, s, parity);
-  const double* rows = P.inlet + (long long)s * P.ny * 4;
-  const double inv2a = 0.5 / c->a;
-  const double gm1 = P.gm1, w = P.w;
-  if (threadIdx.x == 0) mbar_init(&bar);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    mbar_expect_tx(&bar, kAdv2Tx);
-    tma_load_4d(R, parity ? &tma1 : &tma0, &bar, x0 - 2, y0 - 1, 0, s);
-  }
-  mbar_wait(&bar, 0);
-  if (!(x0 >= 2 && x0 + TX2 + 2 <= P.nx && y0 >= 1 && y0 + TY + 1 <= P.ny)) {
-    patch_box<false>(P, src, rows, R, AX2, AY, x0 - 2, y0 - 1, inv2a);
-    __syncthreads();
-  }
-  for (int q = threadIdx.x; q < NA2; q += NT) flux_cell(R, NA2, F, NA2, q, inv2a, gm1, false);
-  __syncthreads();
-
-  const int lane = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int i0 = x0 + 2 * lane, j = y0 + ty;
-  const int q0 = (ty + 1) * AX2 + (2 * lane + 2);  // staged index of cell i0 (even)
-  unsigned long long bits = 0;
-  int bad = 0, nonfin = 0;
-  auto epilogue = [&](const cs& un) {
-    const double sp = signal_speed(un, P.gamma, gm1, P.conservative);
-    if (!isfinite(sp)) {
-      bad = 1;
-    } else {
-      const unsigned long long b = (unsigned long long)__double_as_longlong(sp);
-      bits = b > bits ? b : bits;
-    }
-    if (!finite4(un)) nonfin = 1;
-  };
-  auto M1 = [&](int q, int k) { return staged_m(R, NA2, F, NA2, q, k, w); };
-  const bool interior = x0 >= 1 && x0 + TX2 + 1 <= P.nx && y0 >= 1 && y0 + TY + 1 <= P.ny;
-  if (interior) {  // CTA-uniform: every thread has both cells, all lanes shuffle
-    const long long off = (long long)j * P.pitch + i0;
-    double tw[2], te[2], ts[2], tn[2];
-    if (kMode == 0) {  // interface_theta, solver.hpp:510-534 (interior faces)
-      const double* th = P.theta + (long long)s * P.plane + off;
-      const double2 tc = ld2(th), tS = ld2(th - P.pitch), tN = ld2(th + P.pitch);
-      double tWv = __shfl_up_sync(0xffffffffu, tc.y, 1);
-      double tEv = __shfl_down_sync(0xffffffffu, tc.x, 1);
-      if (lane == 0) tWv = th[-1];
-      if (lane == 31) tEv = th[2];
-      tw[0] = smin(tWv, tc.x), te[0] = smin(tc.x, tc.y);
-      tw[1] = smin(tc.x, tc.y), te[1] = smin(tc.y, tEv);
-      ts[0] = smin(tS.x, tc.x), tn[0] = smin(tc.x, tN.x);
-      ts[1] = smin(tS.y, tc.y), tn[1] = smin(tc.y, tN.y);
-    } else {
-      face_thetas<kMode>(P, s, i0, j, const_theta, tw[0], te[0], ts[0], tn[0]);
-      face_thetas<kMode>(P, s, i0 + 1, j, const_theta, tw[1], te[1], ts[1], tn[1]);
-    }
-    const double* pop = src + 4 * P.plane;  // population k, component c: plane 4k + c
-    double* dpop = dst + 4 * P.plane;
-    const long long pl = P.plane, pl4 = 4 * P.plane;
-    // k = 0 (+x, pulled from the west neighbour)
-    const cs2 P0 = ld_pair4(pop, pl, off);
-    cs W0 = shfl_up4(P0.b, 1);
-    if (lane == 0) W0 = load_plane4(pop, pl, off - 1);
-    const cs2 MC01 = staged_m2(R, F, q0, 0, w);  // M0 at (i0, i0 + 1)
-    const cs M0W = M1(q0 - 1, 0);
-    const cs n1a = add(M0W, scale(tw[0], sub(M0W, W0)));
-    const cs n1b = add(MC01.a, scale(tw[1], sub(MC01.a, P0.a)));
-    st_pair4(dpop, pl, off, n1a, n1b);
-    const cs oTEa = scale(te[0], sub(MC01.a, P0.a)), oTEb = scale(te[1], sub(MC01.b, P0.b));
-    // k = 1 (-x, pulled from the east neighbour)
-    const cs2 P1 = ld_pair4(pop + pl4, pl, off);
-    cs E1 = shfl_down4(P1.a, 1);
-    if (lane == 31) E1 = load_plane4(pop + pl4, pl, off + 2);
-    const cs2 MC11 = staged_m2(R, F, q0, 1, w);  // M1 at (i0, i0 + 1)
-    const cs M1E = M1(q0 + 2, 1);
-    const cs n2a = add(MC11.b, scale(te[0], sub(MC11.b, P1.b)));
-    const cs n2b = add(M1E, scale(te[1], sub(M1E, E1)));
-    st_pair4(dpop + pl4, pl, off, n2a, n2b);
-    const cs sa = add(n1a, n2a), sb = add(n1b, n2b);
-    const cs o1a = add(scale(tw[0], sub(MC11.a, P1.a)), oTEa);
-    const cs o1b = add(scale(tw[1], sub(MC11.b, P1.b)), oTEb);
-    // k = 2 (+y, pulled from the south neighbour)
-    const cs2 S2 = ld_pair4(pop + 2 * pl4, pl, off - P.pitch);
-    const cs2 P2 = ld_pair4(pop + 2 * pl4, pl, off);
-    const cs2 MS2 = staged_m2(R, F, q0 - AX2, 2, w);
-    const cs n3a = add(MS2.a, scale(ts[0], sub(MS2.a, S2.a)));
-    const cs n3b = add(MS2.b, scale(ts[1], sub(MS2.b, S2.b)));
-    st_pair4(dpop + 2 * pl4, pl, off, n3a, n3b);
-    const cs2 MC21 = staged_m2(R, F, q0, 2, w);
-    const cs oTNa = scale(tn[0], sub(MC21.a, P2.a)), oTNb = scale(tn[1], sub(MC21.b, P2.b));
-    // k = 3 (-y, pulled from the north neighbour)
-    const cs2 N3 = ld_pair4(pop + 3 * pl4, pl, off + P.pitch);
-    const cs2 P3 = ld_pair4(pop + 3 * pl4, pl, off);
-    const cs2 MN3 = staged_m2(R, F, q0 + AX2, 3, w);
-    const cs n4a = add(MN3.a, scale(tn[0], sub(MN3.a, N3.a)));
-    const cs n4b = add(MN3.b, scale(tn[1], sub(MN3.b, N3.b)));
-    st_pair4(dpop + 3 * pl4, pl, off, n4a, n4b);
-    const cs2 MC31 = staged_m2(R, F, q0, 3, w);
-    const cs o2a = add(scale(ts[0], sub(MC31.a, P3.a)), oTNa);
-    const cs o2b = add(scale(ts[1], sub(MC31.b, P3.b)), oTNb);
-    // u' = ((n1 + n2) + (n3 + n4)) + alpha u - (...)   (solver.hpp:565-569)
-    const cs2 uc = {plane4(R, NA2, q0), plane4(R, NA2, q0 + 1)};
-    const cs una = sub(add(add(sa, add(n3a, n4a)), scale(P.alpha, uc.a)), add(o1a, o2a));
-    const cs unb = sub(add(add(sb, add(n3b, n4b)), scale(P.alpha, uc.b)), add(o1b, o2b));
-    st_pair4(dst, pl, off, una, unb);
-    epilogue(una);
-    epilogue(unb);
-  } else {
-    for (int h = 0; h < 2; ++h) {
-      const int i = i0 + h;
-      if (i >= P.nx || j >= P.ny) continue;
-      auto gpop = [&](int k, int ii, int jj) {
-        if (ii >= 0 && ii < P.nx && jj >= 0 && jj < P.ny)
-          return load_plane4(src + (4 + 4 * k) * P.plane, P.plane, (long long)jj * P.pitch + ii);
-        return load_pop(P, src, rows, k, ii, jj, inv2a);
-      };
-      double tw, te, ts, tn;
-      face_thetas<kMode>(P, s, i, j, const_theta, tw, te, ts, tn);
-      const long long off = (long long)j * P.pitch + i;
-      const int qc = q0 + h;
-      const cs pw = gpop(0, i - 1, j), pe = gpop(1, i + 1, j), ps = gpop(2, i, j - 1),
-               pn = gpop(3, i, j + 1);
-      const cs M0W = M1(qc - 1, 0), M1E = M1(qc + 1, 1), M2S = M1(qc - AX2, 2),
-               M3N = M1(qc + AX2, 3);
-      const cs n1 = add(M0W, scale(tw, sub(M0W, pw)));
-      const cs n2 = add(M1E, scale(te, sub(M1E, pe)));
-      const cs n3 = add(M2S, scale(ts, sub(M2S, ps)));
-      const cs n4 = add(M3N, scale(tn, sub(M3N, pn)));
-      store_plane4(dst + 4 * P.plane, P.plane, off, n1);
-      store_plane4(dst + 8 * P.plane, P.plane, off, n2);
-      store_plane4(dst + 12 * P.plane, P.plane, off, n3);
-      store_plane4(dst + 16 * P.plane, P.plane, off, n4);
-      cs un = add(add(add(n1, n2), add(n3, n4)), scale(P.alpha, plane4(R, NA2, qc)));
-      const cs P0C = load_plane4(src + 4 * P.plane, P.plane, off);
-      const cs P1C = load_plane4(src + 8 * P.plane, P.plane, off);
-      const cs P2C = load_plane4(src + 12 * P.plane, P.plane, off);
-      const cs P3C = load_plane4(src + 16 * P.plane, P.plane, off);
-      const cs out = add(add(scale(tw, sub(M1(qc, 1), P1C)), scale(te, sub(M1(qc, 0), P0C))),
-                         add(scale(ts, sub(M1(qc, 3), P3C)), scale(tn, sub(M1(qc, 2), P2C))));
-      un = sub(un, out);
-      store_plane4(dst, P.plane, off, un);
-      epilogue(un);
-    }
-  }
-  reduce_signal(c, bits, bad, nonfin);
-}
-
 }  // namespace vlbm_dev
 
 namespace vlbm_impl {
@@ -1111,15 +882,6 @@ static cudaError_t smem_attrs() {
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k_advance_tiled<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)tiled::kAdvanceSmem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k_advance_v2<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)tiled::kAdv2Smem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k_advance_v2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)tiled::kAdv2Smem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k_advance_v2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)tiled::kAdv2Smem);
     return e;
   }();
   if (r == cudaSuccess) done_mask[dev >> 5] |= 1 << (dev & 31);
@@ -1157,7 +919,6 @@ int encode_tensor_maps(MarchParams& P) {
   const cuuint32_t box_adv[4] = {tiled::AX, tiled::AY, 4, 1};
   const cuuint32_t box_thu[4] = {tiled::RX2, tiled::RY2, 4, 1};
   const cuuint32_t box_thp[4] = {tiled::AX, tiled::AY, 16, 1};
-  const cuuint32_t box_adv2[4] = {tiled::AX2, tiled::AY, 4, 1};
   for (int b = 0; b < 2; ++b) {
     void* base = b ? P.buf1 : P.buf0;
     CUresult r = encode(&P.tm_adv[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, base, dims, strides,
@@ -1169,10 +930,6 @@ int encode_tensor_maps(MarchParams& P) {
                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r == CUDA_SUCCESS)
       r = encode(&P.tm_thp[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, base, dims, strides, box_thp,
-                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r == CUDA_SUCCESS)
-      r = encode(&P.tm_adv2[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, base, dims, strides, box_adv2,
                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS)
@@ -1235,29 +992,9 @@ cudaError_t launch_theta_hard(const MarchParams& P, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-// VLBM_ADV=1 (A/B switch): the one-cell-per-thread k_advance_tiled
-static bool use_adv_v1() {
-  static const bool v1 = [] {
-    const char* e = getenv("VLBM_ADV");
-    return e && atoi(e) == 1;
-  }();
-  return v1;
-}
-
 cudaError_t launch_advance_tiled(const MarchParams& P, int mode, double const_theta,
                                  cudaStream_t st) {
   if (cudaError_t e = smem_attrs()) return e;
-  if (!use_adv_v1()) {
-    const dim3 g2((P.nx + tiled::TX2 - 1) / tiled::TX2, (P.ny + tiled::TY - 1) / tiled::TY, P.S);
-    const size_t sm2 = tiled::kAdv2Smem;
-    if (mode == 0)
-      k_advance_v2<0><<<g2, tiled::NT, sm2, st>>>(P, const_theta, P.tm_adv2[0], P.tm_adv2[1]);
-    else if (mode == 1)
-      k_advance_v2<1><<<g2, tiled::NT, sm2, st>>>(P, const_theta, P.tm_adv2[0], P.tm_adv2[1]);
-    else
-      k_advance_v2<2><<<g2, tiled::NT, sm2, st>>>(P, const_theta, P.tm_adv2[0], P.tm_adv2[1]);
-    return cudaGetLastError();
-  }
   const dim3 g = tiled_grid(P);
   const size_t sm = tiled::kAdvanceSmem;
   if (mode == 0)

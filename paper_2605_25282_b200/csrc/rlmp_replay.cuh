@@ -224,7 +224,7 @@ struct Bracket {
 // bisect_finish), else true with the result in br.lo.
 __device__ __forceinline__ bool bisect_replay(const cs& fo, const cs* cf, const cs& delta,
                                               const RlmpBounds& b, const HardStage& h, double gm1,
-                                              int max_exact, Bracket& br, int* audit = nullptr,
+                                              int max_exact, Bracket& br, AuditCtr* audit = nullptr,
                                               int* evals = nullptr) {
   const double thc = h.thc, err = h.err, P0 = h.p0;
   // the concavity arguments need rho > 0 along the diagonal on [0, thc]
@@ -271,7 +271,7 @@ __device__ __forceinline__ bool bisect_replay(const cs& fo, const cs* cf, const 
     const double mid = 0.5 * (lo + hi);
     const int st = status(mid);
     if (st > 1) break;
-    if (audit && (st == 1) != feasible(mid, fo, delta, cf, b, gm1)) atomicAdd(audit, 1);
+    if (audit && (st == 1) != feasible(mid, fo, delta, cf, b, gm1)) atomicAdd(audit, 1ull);
     if (st)
       lo = mid;
     else
@@ -309,7 +309,7 @@ __device__ __forceinline__ bool bisect_replay(const cs& fo, const cs* cf, const 
         }
       }
     }
-    if (audit && ok != feasible(mid, fo, delta, cf, b, gm1)) atomicAdd(audit, 1);
+    if (audit && ok != feasible(mid, fo, delta, cf, b, gm1)) atomicAdd(audit, 1ull);
     if (ok)
       lo = mid;
     else
@@ -323,11 +323,11 @@ __device__ __forceinline__ bool bisect_replay(const cs& fo, const cs* cf, const 
 // exactly (the vertices outside `unc` pass on [0, thc]).
 __device__ __forceinline__ double bisect_finish(const cs& fo, const cs* cf, const cs& delta,
                                                 const RlmpBounds& b, unsigned unc, Bracket br,
-                                                double gm1, int* audit = nullptr) {
+                                                double gm1, AuditCtr* audit = nullptr) {
   for (int it = br.it; it < 30; ++it) {
     const double mid = 0.5 * (br.lo + br.hi);
     const bool ok = feasible_unc(mid, fo, delta, cf, b, unc, gm1);
-    if (audit && ok != feasible(mid, fo, delta, cf, b, gm1)) atomicAdd(audit, 1);
+    if (audit && ok != feasible(mid, fo, delta, cf, b, gm1)) atomicAdd(audit, 1ull);
     if (ok)
       br.lo = mid;
     else
@@ -340,7 +340,7 @@ __device__ __forceinline__ double bisect_finish(const cs& fo, const cs* cf, cons
 // the replayed bisection.
 __device__ __forceinline__ double rlmp_theta_hard_replay(const cs& fo, const cs* cf,
                                                          const RlmpBounds& b, double gm1,
-                                                         int* audit = nullptr) {
+                                                         AuditCtr* audit = nullptr) {
   const cs delta = add(add(cf[0], cf[1]), add(cf[2], cf[3]));
   if (!(finite4(fo) && finite4(cf[0]) && finite4(cf[1]) && finite4(cf[2]) && finite4(cf[3]) &&
         finite4(delta)))
@@ -348,8 +348,8 @@ __device__ __forceinline__ double rlmp_theta_hard_replay(const cs& fo, const cs*
   const HardStage h = rlmp_hard_stage(fo, cf, delta, b, gm1);
   if (h.done) return h.result;
   if (audit) {  // statistics: [1] bisections, [2] certified at thc, [3] uncertified
-    atomicAdd(audit + 1, 1);
-    atomicAdd(audit + (h.unc ? 3 : 2), 1);
+    atomicAdd(audit + 1, 1ull);
+    atomicAdd(audit + (h.unc ? 3 : 2), 1ull);
   }
   Bracket br;
   bisect_replay(fo, cf, delta, b, h, gm1, 30, br, audit);

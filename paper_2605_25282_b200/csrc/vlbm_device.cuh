@@ -12,6 +12,9 @@
 
 namespace vlbm_dev {
 
+// 64-bit audit counters (test hook; production-scale runs exceed 2^32 events)
+using AuditCtr = unsigned long long;
+
 struct cs {  // ConservedState, euler.hpp:16-46 (rho, mom_x, mom_y, energy)
   double r, mx, my, e;
 };

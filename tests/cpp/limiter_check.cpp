@@ -27,8 +27,8 @@ static inline double __longlong_as_double(long long x) {
   std::memcpy(&d, &x, 8);
   return d;
 }
-static inline int atomicAdd(int* p, int v) {
-  const int o = *p;
+static inline unsigned long long atomicAdd(unsigned long long* p, unsigned long long v) {
+  const unsigned long long o = *p;
   *p += v;
   return o;
 }
@@ -49,7 +49,7 @@ int main(int argc, char** argv) {
   double r[27];
   long cells = 0, at_one = 0, cert = 0, cert_bad = 0, hard = 0, bisect = 0, stopped = 0;
   long bad_plain = 0, bad_queued = 0, bad_replay = 0, margin_bad = 0;
-  int audit[16] = {0};
+  unsigned long long audit[16] = {0};
   while (std::fread(r, sizeof r, 1, f) == 1) {
     ++cells;
     const cs fo = {r[0], r[1], r[2], r[3]};
@@ -129,7 +129,7 @@ int main(int argc, char** argv) {
   std::printf(
       "{\"cells\": %ld, \"theta_one\": %ld, \"certified_at_one\": %ld, \"certificate_errors\": %ld, "
       "\"hard\": %ld, \"bisections\": %ld, \"replay_stopped\": %ld, \"mismatch_plain\": %ld, "
-      "\"mismatch_queued\": %ld, \"mismatch_replay\": %ld, \"audit_errors\": %d, "
+      "\"mismatch_queued\": %ld, \"mismatch_replay\": %ld, \"audit_errors\": %llu, "
       "\"margin_errors\": %ld, \"hypot_checks\": %ld, \"hypot_errors\": %ld}\n",
       cells, at_one, cert, cert_bad, hard, bisect, stopped, bad_plain, bad_queued, bad_replay,
       audit[0], margin_bad, hyp_n, hyp_bad);
