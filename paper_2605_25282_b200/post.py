@@ -96,3 +96,30 @@ def strong_finish(partials) -> float:
 def strong_error(torch, coarse, fine) -> float:
     """strong_error(coarse, restrict(fine)) when only this variable is nonzero."""
     return strong_finish(strong_partials(torch, coarse, fine).cpu().numpy())
+
+
+def pair_metrics(coarse, fine, var: int = 0, batch: int = 0, device: int = 0):
+    """compute_metrics' (W1, E_strong) of one grid pair and time through the
+    C ABI's vlbm_metrics_* (one upload per ensemble, restriction fused, all
+    reductions on the device): host fields coarse (M, 4, nyc, nxc), fine
+    (M, 4, 2 nyc, 2 nxc), added in batches of ``batch`` samples (0: all)."""
+    c = np.ascontiguousarray(coarse, np.float64)
+    f = np.ascontiguousarray(fine, np.float64)
+    M, _, nyc, nxc = c.shape
+    if f.shape != (M, 4, 2 * nyc, 2 * nxc):
+        raise ValueError("wasserstein1: inconsistent field sizes")
+    L = lib()
+    h = C.c_void_p()
+    _check(L.vlbm_metrics_begin(M, nxc, nyc, int(var), device, C.byref(h)))
+    try:
+        b = batch or M
+        dp = C.POINTER(C.c_double)
+        for s0 in range(0, M, b):
+            nb = min(b, M - s0)
+            _check(L.vlbm_metrics_add(h, s0, nb, c[s0:s0 + nb].ctypes.data_as(dp),
+                                      f[s0:s0 + nb].ctypes.data_as(dp)))
+        w1, es = C.c_double(), C.c_double()
+        _check(L.vlbm_metrics_finish(h, C.byref(w1), C.byref(es), None))
+        return w1.value, es.value
+    finally:
+        L.vlbm_metrics_destroy(h)

@@ -232,3 +232,107 @@ def _sharded_metrics(torch, dist, group, grids, times, store, valid, k, rep, w1s
     if rank != 0:
         return None
     return _finish_rates(rep, grids, times, w1s, strongs)
+
+
+def production_sweep(torch, nx0: int, ny0: int, levels: int, n_samples: int,
+                     times: Sequence[float], base_seed: int = 42, batch: int = 125,
+                     lattice: LatticeParams = LatticeParams(), gas: GasParams = GasParams(),
+                     pp: PerturbationParams = PerturbationParams(), strip_width: float = 0.02,
+                     metric_variable: int = 0, m0: int = 0, device: int = 0,
+                     progress=None) -> SweepReport:
+    """grid_sweep at production scale (BASELINE configs[4]: M = 1000, grids up
+    to 2000x400 / 4000x800): the same rows and rates, bit for bit, without
+    keeping every level's snapshots.
+
+    Sample-batch major: each batch of samples is marched on every level in
+    turn (level l's snapshots of the batch stay on the device only until
+    level l + 1 of the batch has run).  As soon as a fine-level snapshot of
+    the batch exists, the pair's per-sample strong_error partials are taken
+    against the coarse snapshot (restriction fused, vlbm_d_strong_partials),
+    and the metric variable is kept for W1 -- the coarse plane and the
+    restricted fine plane (vlbm_d_restrict_var: the same arithmetic as the
+    fused restriction).  After the last batch: joint validity per pair, W1 of
+    the jointly valid samples per (pair, time) on the device (cell terms +
+    storage-order mean), E_strong from their partials in sample order, and
+    the rate fits.  Device memory: one level's batch state, the previous
+    level's batch snapshots and the W1 planes (2 x M x coarse cells per
+    pair and time)."""
+    if levels < 2:
+        raise RuntimeError("metrics: need >= 2 grids for Cauchy errors")
+    import time as _time
+    times = list(times)
+    T, M = len(times), n_samples
+    dev = torch.device("cuda", device)
+    grids = [Grid(nx0 << l, ny0 << l) for l in range(levels)]
+    k = metric_variable
+    f64 = torch.float64
+    # W1 planes [pair][time]: coarse plane (M, nc) and restricted fine plane (M, nc)
+    w1c = [[torch.empty((M, grids[p].cells()), dtype=f64, device=dev) for _ in times]
+           for p in range(levels - 1)]
+    w1f = [[torch.empty((M, grids[p].cells()), dtype=f64, device=dev) for _ in times]
+           for p in range(levels - 1)]
+    part = [torch.empty((T, M, 10), dtype=f64, device=dev) for _ in range(levels - 1)]
+    valid = [np.ones(M, bool) for _ in grids]
+    steps = [np.zeros(M, np.int64) for _ in grids]
+    march_s = [0.0] * levels
+    rep = SweepReport()
+    stream = torch.cuda.current_stream(dev)
+    for b0 in range(0, M, batch):
+        nb = min(batch, M - b0)
+        prev = None  # level l-1 snapshots of this batch: (T, nb, 4, ny, nx)
+        for l, g in enumerate(grids):
+            keep = l < levels - 1
+            cur = torch.empty((T if keep else 1, nb, 4, g.ny, g.nx), dtype=f64, device=dev)
+            t0 = _time.perf_counter()
+            with BatchSimulation.jet(g, lattice, gas, pp, base_seed, m0 + b0, nb, strip_width,
+                                     device) as sim:
+                for ti, t in enumerate(times):
+                    sim.run_to(t)
+                    buf = cur[ti if keep else 0]
+                    sim.fields_to_device(buf.data_ptr())
+                    torch.cuda.synchronize(dev)
+                    s = stream.cuda_stream
+                    if l > 0:
+                        cg = grids[l - 1]
+                        _check(lib().vlbm_d_strong_partials(
+                            nb, cg.nx, cg.ny, prev[ti].data_ptr(), buf.data_ptr(),
+                            part[l - 1][ti, b0:b0 + nb].data_ptr(), s))
+                        _check(lib().vlbm_d_restrict_var(
+                            nb, cg.nx, cg.ny, buf.data_ptr(), k,
+                            w1f[l - 1][ti][b0:b0 + nb].data_ptr(), s))
+                    if keep:
+                        w1c[l][ti][b0:b0 + nb].copy_(buf[:, k].reshape(nb, -1))
+                _, st, status = sim.scalars()
+            torch.cuda.synchronize(dev)
+            march_s[l] += _time.perf_counter() - t0
+            valid[l][b0:b0 + nb] &= status != 2
+            steps[l][b0:b0 + nb] = st
+            prev = cur if keep else None
+            if progress:
+                progress(b0 + nb, M, g.label())
+    for l, g in enumerate(grids):
+        rep.steps[g.label()] = steps[l]
+    rep.march_seconds = {g.label(): march_s[l] for l, g in enumerate(grids)}
+    n_pairs = levels - 1
+    w1s = [[0.0] * T for _ in range(n_pairs)]
+    strongs = [[0.0] * T for _ in range(n_pairs)]
+    t0 = _time.perf_counter()
+    for p in range(n_pairs):
+        cg, fg = grids[p], grids[p + 1]
+        mask = valid[p] & valid[p + 1]
+        m_star = int(mask.sum())
+        if m_star < 1:
+            raise RuntimeError("metrics: no jointly valid samples for pair")
+        idx = torch.from_numpy(np.flatnonzero(mask)).to(dev)
+        for ti, t in enumerate(times):
+            a = w1c[p][ti].index_select(0, idx).contiguous()
+            b = w1f[p][ti].index_select(0, idx).contiguous()
+            terms = torch.empty(cg.cells(), dtype=f64, device=dev)
+            _check(lib().vlbm_d_w1_cells_planes(m_star, cg.cells(), a.data_ptr(), b.data_ptr(),
+                                                terms.data_ptr(), stream.cuda_stream))
+            w1 = float(post.ordered_mean(torch, terms).item())
+            es = post.strong_finish(part[p][ti].index_select(0, idx).cpu().numpy())
+            rep.rows.append(MetricsRow(float(t), f"{cg.nx}->{fg.nx}", m_star, w1, es))
+            w1s[p][ti], strongs[p][ti] = w1, es
+    rep.metrics_seconds = _time.perf_counter() - t0
+    return _finish_rates(rep, grids, times, w1s, strongs)

@@ -187,6 +187,10 @@ def lib() -> C.CDLL:
     sig("vlbm_batch_set_audit", I, [V, I])
     sig("vlbm_batch_audit", I, [V, C.POINTER(I64)])
     sig("vlbm_batch_queue_stats", I, [V, C.POINTER(I64)])
+    sig("vlbm_metrics_begin", I, [I, I, I, I, I, C.POINTER(V)])
+    sig("vlbm_metrics_add", I, [V, I, I, DP, DP])
+    sig("vlbm_metrics_finish", I, [V, DP, DP, DP])
+    sig("vlbm_metrics_destroy", None, [V])
     sig("vlbm_restrict_field", I, [I, I, DP, DP])
     sig("vlbm_strong_error", I, [I, I64, DP, DP, DP, DP])
     sig("vlbm_wasserstein1", I, [I, I64, DP, DP, I, DP])

@@ -165,3 +165,34 @@ def test_device_pipeline_c4_style(vlbm, oc, M, nxc, nyc, monkeypatch):
     R4 = np.stack([oc.restrict_field(F4[m]) for m in range(M)])
     assert bits(w1) == bits(oc.wasserstein1(C4, R4, 0))
     assert bits(es) == bits(oc.strong_error(C4, R4)[0])
+
+
+@pytest.mark.parametrize("nyc,nxc", [(4, 2000), (16, 250)])
+def test_config4_slice_w1_l1_vs_reference(vlbm, nyc, nxc):
+    """BASELINE configs[3] on a slice (M = 1000 log-normal density samples,
+    mean 1, sigma 0.5; the other components zero): nyc coarse rows of nxc
+    cells against the restriction of 2 nyc x 2 nxc fine rows.  W1 through the
+    production call (vlbm_d_w1_restrict_mean: restriction fused, the 16-chunk
+    storage-order mean overlapped on a second stream -- 16 chunks when
+    nyc >= 16) and E_strong (device partials), and both again through
+    vlbm_metrics_* (compute_metrics' one-upload path, in batches), all
+    bit-identical to the reference's restrict_field + wasserstein1 +
+    strong_error (ref_postproc_timed: compute_metrics' calls)."""
+    import torch
+    from oracle import oracle
+    if not oracle.available("ref"):
+        pytest.skip("oracle/_ref not built")
+    from paper_2605_25282_b200 import post
+    M = 1000
+    rng = np.random.default_rng(nyc * 7 + nxc)
+    coarse = np.zeros((M, 4, nyc, nxc))
+    fine = np.zeros((M, 4, 2 * nyc, 2 * nxc))
+    coarse[:, 0] = rng.lognormal(-0.125, 0.5, size=(M, nyc, nxc))
+    fine[:, 0] = rng.lognormal(-0.125, 0.5, size=(M, 2 * nyc, 2 * nxc))
+    _, w1_ref, es_ref = oracle.Oracle("ref").postproc_timed(coarse, fine)
+    c = torch.from_numpy(np.ascontiguousarray(coarse[:, 0])).cuda()
+    f = torch.from_numpy(np.ascontiguousarray(fine[:, 0])).cuda()
+    assert bits(post.wasserstein1(torch, c, f)) == bits(w1_ref)
+    assert bits(post.strong_error(torch, c, f)) == bits(es_ref)
+    w1m, esm = post.pair_metrics(coarse, fine, var=0, batch=300)
+    assert bits(w1m) == bits(w1_ref) and bits(esm) == bits(es_ref)

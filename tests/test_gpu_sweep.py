@@ -105,3 +105,26 @@ def test_grid_sweep_sharded_equals_single_process():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert got == want
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("batch", [2, 4, 6])
+def test_production_sweep_equals_grid_sweep(vlbm, batch):
+    """The production sweep (sample-batch major, only the W1 planes and the
+    strong_error partials kept) gives grid_sweep's rows, rates and step
+    counts bit for bit -- grid_sweep being pinned to the reference's
+    run_sample + compute_metrics above -- for several batch splits."""
+    from paper_2605_25282_b200 import sweep
+    nx0, ny0, levels, M = 60, 12, 3, 6
+    times = [0.0, 3e-4, 6e-4]
+    want = sweep.grid_sweep(torch, nx0, ny0, levels, M, times, base_seed=42)
+    got = sweep.production_sweep(torch, nx0, ny0, levels, M, times, base_seed=42, batch=batch)
+    assert len(got.rows) == len(want.rows)
+    for a, b in zip(got.rows, want.rows):
+        assert (a.time, a.pair, a.m_star) == (b.time, b.pair, b.m_star)
+        assert bits(a.w1) == bits(b.w1) and bits(a.e_strong) == bits(b.e_strong), (a, b)
+    for a, b in zip(got.rates, want.rates):
+        for x, y in ((a.r_w1, b.r_w1), (a.r_strong, b.r_strong)):
+            assert (np.isnan(x) and np.isnan(y)) or bits(x) == bits(y)
+    for lab in want.steps:
+        assert list(got.steps[lab]) == list(want.steps[lab])
