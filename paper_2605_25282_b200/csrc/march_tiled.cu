@@ -425,7 +425,11 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_THETA_MINB)
                                                                b.p_floor, gm1,
                                                                P.audit ? parts : nullptr);
         need = !cert;
+#ifdef VLBM_EXP_NOVERTEX  // timing experiment only (WRONG results): the vertex checks' share
+        const bool ok = true;
+#else
         const bool ok = cert || vertex_floors_ok(1.0, foC, cf, b, gm1);
+#endif
         if (P.audit) {  // [8] diagonal passed, [9] certified, [10] feasible; [0] certificate errors
           aflags |= 1u << 8;
           if (cert) aflags |= 1u << 9;

@@ -3,8 +3,11 @@
 Every comparison is BIT-EXACT (uint64 views, so +-0 and NaN payloads count):
 the limiter's discrete decisions amplify one ulp to O(1) within ~50 steps
 (SURVEY.md §0 fact 4), so anything short of bit identity is a failure.  The
-oracle (oracle/vlbm_oracle.c) is itself pinned bit-for-bit to the reference
-(tests/test_oracle_pin.py).
+oracle is the reference itself (`orc`: oracle/_ref, the unmodified headers
+compiled by oracle/Makefile, whose .so travels to the GPU box) whenever it is
+built, else the C restatement (oracle/vlbm_oracle.c, pinned bit-for-bit to
+the reference by tests/test_oracle_pin.py); the cell-theta checks use the
+restatement (the reference does not expose its cell theta).
 """
 import numpy as np
 import pytest
@@ -33,13 +36,14 @@ def assert_bitwise(got, want, what):
 
 # ---- config 1: 200x40, M=8, 200 steps of step(suggest_dt()) -----------------
 
-def test_config1_bitwise_per_step(vlbm, vo):
+def test_config1_bitwise_per_step(vlbm, orc, vo):
     """BASELINE configs[0]: every sample's u, pops and cell theta bit-identical
     to the oracle after steps 1, 2, 5, 20, 50, 100 and 200."""
     g = vlbm.Grid(200, 40)
     M = 8
     sim = vlbm.BatchSimulation.jet(g, n_samples=M, base_seed=42)
-    refs = [vo.jet_sim(make_grid(200, 40), make_params(), make_pert(), 42, m) for m in range(M)]
+    refs = [orc.jet_sim(make_grid(200, 40), make_params(), make_pert(), 42, m) for m in range(M)]
+    th_refs = [vo.jet_sim(make_grid(200, 40), make_params(), make_pert(), 42, m) for m in (0, 5)]
     done = 0
     for target in (1, 2, 5, 20, 50, 100, 200):
         sim.step(target - done)
@@ -54,8 +58,10 @@ def test_config1_bitwise_per_step(vlbm, vo):
             u, p = r.get(pops=True)
             assert_bitwise(sim.state(m), u, f"u sample {m} step {target}")
             assert_bitwise(sim.populations(m), p, f"pops sample {m} step {target}")
-    # cell theta of the last step (oracle keeps it after the step)
-    for m, r in enumerate(refs):
+    # cell theta of the last step (the restatement keeps it after the step)
+    for m, r in zip((0, 5), th_refs):
+        for _ in range(200):
+            r.step(r.suggest_dt())
         assert_bitwise(sim.theta_cell(m), r.theta_cell(), f"theta sample {m}")
 
 
@@ -79,7 +85,7 @@ def test_ragged_grids_bitwise(vlbm, vo, nx, ny):
         assert_bitwise(sim.theta_cell(m), r.theta_cell(), f"theta {nx}x{ny} sample {m}")
 
 
-def test_run_samples_matches_run_sample(vlbm, vo):
+def test_run_samples_matches_run_sample(vlbm, orc):
     """run_samples == run_sample for every snapshot of 3 samples on the smoke
     grid 125x25 to t_end = 0.003 (times, diverged flags, steps, fields)."""
     times = [0.0, 0.00075, 0.0015, 0.00225, 0.003]
@@ -87,7 +93,7 @@ def test_run_samples_matches_run_sample(vlbm, vo):
     res = vlbm.run_samples(g, vlbm.LatticeParams(), vlbm.GasParams(), vlbm.PerturbationParams(),
                            42, 0, 3, 0.02, times)
     for m in range(3):
-        want = vo.run_sample(make_grid(125, 25), make_params(), make_pert(), 42, m, times)
+        want = orc.run_sample(make_grid(125, 25), make_params(), make_pert(), 42, m, times)
         r = res[m]
         assert r.steps == want["steps"] and r.admissible == want["admissible"]
         for ti in range(len(times)):
@@ -97,7 +103,7 @@ def test_run_samples_matches_run_sample(vlbm, vo):
             assert_bitwise(s.data, want["fields"][ti], f"snapshot m={m} t={ti}")
 
 
-def test_samples_not_in_lockstep(vlbm, vo):
+def test_samples_not_in_lockstep(vlbm, orc):
     """Samples keep their own dt: a batch that starts at m0=5 reproduces the
     oracle's samples 5..8 (different step counts to the same target)."""
     g = vlbm.Grid(100, 20)
@@ -105,7 +111,7 @@ def test_samples_not_in_lockstep(vlbm, vo):
     sim.run_to(0.0004)
     t, steps, status = sim.scalars()
     for s in range(4):
-        r = vo.jet_sim(make_grid(100, 20), make_params(), make_pert(), 7, 5 + s)
+        r = orc.jet_sim(make_grid(100, 20), make_params(), make_pert(), 7, 5 + s)
         n = 0
         while r.time < 0.0004 - 1e-12:
             r.step(min(r.suggest_dt(), 0.0004 - r.time))
@@ -142,7 +148,7 @@ BC_CASES = {
 
 @pytest.mark.parametrize("case", list(BC_CASES))
 @pytest.mark.parametrize("limiter", [RLMP, FIRST_ORDER, SECOND_ORDER])
-def test_boundary_variants_bitwise(vlbm, vo, case, limiter):
+def test_boundary_variants_bitwise(vlbm, orc, case, limiter):
     bc, nx, ny = BC_CASES[case]
     x_max = 0.5 * nx / ny
     init = smooth_field(nx, ny, x_max)
@@ -154,7 +160,7 @@ def test_boundary_variants_bitwise(vlbm, vo, case, limiter):
     lat = vlbm.LatticeParams(limiter=vlbm.Limiter(limiter))
     bcs = vlbm.Boundaries(*[vlbm.BcType(b) for b in bc])
     sim = vlbm.BatchSimulation(g, lat, vlbm.GasParams(gamma), bcs, init)
-    r = vo.sim(make_grid(nx, ny, x_max), make_params(gamma=gamma, limiter=limiter, bc=bc), init)
+    r = orc.sim(make_grid(nx, ny, x_max), make_params(gamma=gamma, limiter=limiter, bc=bc), init)
     for n in (1, 4, 15):
         sim.step(n)
         for _ in range(n):
@@ -164,17 +170,17 @@ def test_boundary_variants_bitwise(vlbm, vo, case, limiter):
         assert_bitwise(sim.populations(0), p, f"{case} pops")
 
 
-def test_inlet_generic_fields_and_alpha(vlbm, vo):
+def test_inlet_generic_fields_and_alpha(vlbm, orc):
     """Generic construction with inlet rows and alpha = 0.25 (M5 = alpha u)."""
     nx, ny = 60, 12
     g = vlbm.Grid(nx, ny)
     pp = make_pert()
-    seed, yc, zc = vo.draw_coefficients(3, 1, 10)
-    rows = vo.inlet_rows(make_grid(nx, ny), yc, zc, pp)
-    init = vo.initial_field(make_grid(nx, ny), yc, zc, pp, strip=0.1)
+    seed, yc, zc = orc.draw_coefficients(3, 1, 10)
+    rows = orc.inlet_rows(make_grid(nx, ny), yc, zc, pp)
+    init = orc.initial_field(make_grid(nx, ny), yc, zc, pp, strip=0.1)
     lat = vlbm.LatticeParams(alpha=0.25)
     sim = vlbm.BatchSimulation(g, lat, vlbm.GasParams(), vlbm.Boundaries(), init, rows)
-    r = vo.sim(make_grid(nx, ny), make_params(alpha=0.25), init, rows)
+    r = orc.sim(make_grid(nx, ny), make_params(alpha=0.25), init, rows)
     sim.step(30)
     for _ in range(30):
         r.step(r.suggest_dt())
@@ -183,13 +189,13 @@ def test_inlet_generic_fields_and_alpha(vlbm, vo):
     assert_bitwise(sim.populations(0), p, "alpha pops")
 
 
-def test_fixed_dt_steps(vlbm, vo):
+def test_fixed_dt_steps(vlbm, orc):
     nx, ny = 40, 8
     init = smooth_field(nx, ny, 0.5 * nx / ny)
     g = vlbm.Grid(nx, ny, 0.5 * nx / ny)
     bcs = vlbm.Boundaries(*[vlbm.BcType.Periodic] * 4)
     sim = vlbm.BatchSimulation(g, vlbm.LatticeParams(), vlbm.GasParams(1.4), bcs, init)
-    r = vo.sim(make_grid(nx, ny, 0.5 * nx / ny), make_params(gamma=1.4, bc=(3, 3, 3, 3)), init)
+    r = orc.sim(make_grid(nx, ny, 0.5 * nx / ny), make_params(gamma=1.4, bc=(3, 3, 3, 3)), init)
     dt = 0.7 * r.suggest_dt()
     sim.step(10, dt=dt)
     for _ in range(10):
@@ -197,7 +203,7 @@ def test_fixed_dt_steps(vlbm, vo):
     assert_bitwise(sim.state(0), r.get(), "fixed dt")
 
 
-def test_step_with_blending_random(vlbm, vo):
+def test_step_with_blending_random(vlbm, orc):
     """step_with_blending (solver.hpp:173-181) with random interface thetas."""
     nx, ny = 16, 16
     x_max = 0.5
@@ -205,7 +211,7 @@ def test_step_with_blending_random(vlbm, vo):
     g = vlbm.Grid(nx, ny, x_max)
     bcs = vlbm.Boundaries(*[vlbm.BcType.Periodic] * 4)
     sim = vlbm.BatchSimulation(g, vlbm.LatticeParams(), vlbm.GasParams(1.4), bcs, init)
-    r = vo.sim(make_grid(nx, ny, x_max), make_params(gamma=1.4, bc=(3, 3, 3, 3)), init)
+    r = orc.sim(make_grid(nx, ny, x_max), make_params(gamma=1.4, bc=(3, 3, 3, 3)), init)
     rng = np.random.default_rng(5)
     for _ in range(5):
         tx = rng.random((ny, nx + 1))
@@ -272,7 +278,7 @@ def test_mirror_symmetry_unperturbed_jet(vlbm):
     assert np.abs(s[0] - 0.5).sum() > 1.0
 
 
-def test_divergence_flags_like_run_sample(vlbm, vo):
+def test_divergence_flags_like_run_sample(vlbm, orc):
     """A blow-up (tiny safety factor, no limiter) is an outcome, not an error:
     the sample stops, later snapshots are placeholders with the sample's own
     time, exactly as run_sample (solver.hpp:645-666)."""
@@ -282,7 +288,7 @@ def test_divergence_flags_like_run_sample(vlbm, vo):
     res = vlbm.run_samples(g, lat, vlbm.GasParams(), vlbm.PerturbationParams(), 42, 0, 2, 0.02,
                            times)
     for m in range(2):
-        want = vo.run_sample(make_grid(60, 12), make_params(limiter=SECOND_ORDER, safety=1.0),
+        want = orc.run_sample(make_grid(60, 12), make_params(limiter=SECOND_ORDER, safety=1.0),
                              make_pert(), 42, m, times)
         assert res[m].admissible == want["admissible"]
         assert res[m].steps == want["steps"]
@@ -293,7 +299,7 @@ def test_divergence_flags_like_run_sample(vlbm, vo):
             assert_bitwise(s.data, want["fields"][ti], f"diverging sample {m} t{ti}")
 
 
-def test_certified_bisection_audit_and_late_time_parity(vlbm, vo):
+def test_certified_bisection_audit_and_late_time_parity(vlbm, orc):
     """The limiter's certified bisection (rlmp.cuh) skips the vertex floors
     only where a rigorous rounding bound proves they pass.  With the audit on,
     every certified step is re-run in full on the GPU: zero disagreements over
@@ -305,7 +311,7 @@ def test_certified_bisection_audit_and_late_time_parity(vlbm, vo):
     assert sim.audit_mismatches() == 0
     t, steps, status = sim.scalars()
     for m in (0, 5):
-        r = vo.jet_sim(make_grid(300, 60), make_params(), make_pert(), 42, m)
+        r = orc.jet_sim(make_grid(300, 60), make_params(), make_pert(), 42, m)
         while r.time < 0.0009 - 1e-12:
             r.step(min(r.suggest_dt(), 0.0009 - r.time))
         assert steps[m] == r.steps
@@ -313,7 +319,7 @@ def test_certified_bisection_audit_and_late_time_parity(vlbm, vo):
 
 
 @pytest.mark.parametrize("cap", ["1536", "0"])
-def test_limiter_queue_overflow_paths_bitwise(vlbm, vo, monkeypatch, cap):
+def test_limiter_queue_overflow_paths_bitwise(vlbm, orc, monkeypatch, cap):
     """A limiter queue far smaller than the hard cells (VLBM_HQ_CAP test hook):
     CTAs whose cells do not fit finish them in place (tile pass, stage,
     bisection tail) -- and with no queue at all (cap 0) every hard cell is
@@ -325,7 +331,7 @@ def test_limiter_queue_overflow_paths_bitwise(vlbm, vo, monkeypatch, cap):
     sim.run_to(0.0008)
     t, steps, status = sim.scalars()
     for m in (0, 3):
-        r = vo.jet_sim(make_grid(200, 40), make_params(), make_pert(), 42, m)
+        r = orc.jet_sim(make_grid(200, 40), make_params(), make_pert(), 42, m)
         while r.time < 0.0008 - 1e-12:
             r.step(min(r.suggest_dt(), 0.0008 - r.time))
         assert steps[m] == r.steps
@@ -365,7 +371,7 @@ def test_serial_sample_groups_bitwise(vlbm, orc, monkeypatch, groups, cap):
 
 
 @pytest.mark.parametrize("limiter", [RLMP, FIRST_ORDER])
-def test_sod_tube_bitwise(vlbm, vo, limiter):
+def test_sod_tube_bitwise(vlbm, orc, limiter):
     """test_riemann.cpp's Sod tube (gamma 1.4; left rho 1, p 1, right rho
     0.125, p 0.1, at rest) on a 400x4 strip with outflow x and periodic y:
     shock, contact and rarefaction through the limiter; fields bit-identical
@@ -385,7 +391,7 @@ def test_sod_tube_bitwise(vlbm, vo, limiter):
     lat = vlbm.LatticeParams(limiter=vlbm.Limiter(limiter))
     bcs = vlbm.Boundaries(*[vlbm.BcType(b) for b in bc])
     sim = vlbm.BatchSimulation(g, lat, vlbm.GasParams(gamma), bcs, init)
-    r = vo.sim(make_grid(nx, ny, x_max), make_params(gamma=gamma, limiter=limiter, bc=bc), init)
+    r = orc.sim(make_grid(nx, ny, x_max), make_params(gamma=gamma, limiter=limiter, bc=bc), init)
     sim.step(300)
     for _ in range(300):
         r.step(r.suggest_dt())
@@ -397,7 +403,7 @@ def test_sod_tube_bitwise(vlbm, vo, limiter):
 
 @pytest.mark.parametrize("kappa,safety,floor,cons", [(0.25, 2.5, 1e-6, 1), (0.9, 3.0, 1e-9, 0),
                                                       (0.0, 2.0, 1e-7, 1)])
-def test_jet_lattice_parameters_bitwise(vlbm, vo, kappa, safety, floor, cons):
+def test_jet_lattice_parameters_bitwise(vlbm, orc, kappa, safety, floor, cons):
     """Non-default lattice parameters of the jet (lattice.hpp:13-35): RLMP
     relaxation kappa, the dt safety factor, the positivity floor and the
     conservative (hypot) signal-speed bound; 60 steps of 2 samples, fields
@@ -410,7 +416,7 @@ def test_jet_lattice_parameters_bitwise(vlbm, vo, kappa, safety, floor, cons):
     t, _, _ = sim.scalars()
     p = make_params(safety=safety, kappa=kappa, floor=floor, conservative_bound=cons)
     for m in range(2):
-        r = vo.jet_sim(make_grid(200, 40), p, make_pert(), 3, m)
+        r = orc.jet_sim(make_grid(200, 40), p, make_pert(), 3, m)
         for _ in range(60):
             r.step(r.suggest_dt())
         assert bits(t[m]) == bits(r.time)
@@ -419,7 +425,7 @@ def test_jet_lattice_parameters_bitwise(vlbm, vo, kappa, safety, floor, cons):
         assert_bitwise(sim.populations(m), pops, f"pops sample {m}")
 
 
-def test_jet_perturbation_parameters_bitwise(vlbm, vo):
+def test_jet_perturbation_parameters_bitwise(vlbm, orc):
     """Non-default jet / perturbation parameters (perturbation.hpp:16-31:
     amplitude, modes, decay, jet radius, density and speed, ambient state)
     and inlet strip width: 50 steps of 3 samples, fields and times
@@ -433,7 +439,7 @@ def test_jet_perturbation_parameters_bitwise(vlbm, vo):
     sim.step(50)
     t, _, _ = sim.scalars()
     for s in range(3):
-        r = vo.jet_sim(make_grid(160, 32), make_params(), make_pert(**kw), 9, 4 + s, strip=0.05)
+        r = orc.jet_sim(make_grid(160, 32), make_params(), make_pert(**kw), 9, 4 + s, strip=0.05)
         for _ in range(50):
             r.step(r.suggest_dt())
         assert bits(t[s]) == bits(r.time)
@@ -442,7 +448,7 @@ def test_jet_perturbation_parameters_bitwise(vlbm, vo):
         assert_bitwise(sim.populations(s), pops, f"pops sample {4 + s}")
 
 
-def test_config2_first_50_steps_bitwise(vlbm, vo):
+def test_config2_first_50_steps_bitwise(vlbm, orc):
     """BASELINE configs[1]'s parity statement: per-sample fields of the
     1000x200 jet equal the CPU oracle for the first 50 steps (here every bit,
     4 of the 64 samples: 0, 21, 42, 63 of a 64-sample batch)."""
@@ -451,7 +457,7 @@ def test_config2_first_50_steps_bitwise(vlbm, vo):
     sim.step(50)
     t, steps, _ = sim.scalars()
     for m in (0, 21, 42, 63):
-        r = vo.jet_sim(make_grid(1000, 200), make_params(), make_pert(), 42, m)
+        r = orc.jet_sim(make_grid(1000, 200), make_params(), make_pert(), 42, m)
         for _ in range(50):
             r.step(r.suggest_dt())
         assert steps[m] == 50 and bits(t[m]) == bits(r.time)
@@ -510,7 +516,7 @@ def test_unsupported_x_boundaries_rejected(vlbm, bc):
 
 
 @pytest.mark.parametrize("alpha", [0.5, 0.9])
-def test_rest_population_weight_bitwise(vlbm, vo, alpha):
+def test_rest_population_weight_bitwise(vlbm, orc, alpha):
     """alpha in (0, 1) (test_lattice.cpp:31-49: M5 = alpha u, w = (1 - alpha)/4):
     periodic smooth field with a spike, RLMP, 10 steps bit-identical to the
     oracle.  (With this spike alpha = 0.9 becomes inadmissible at step 14 and
@@ -525,7 +531,7 @@ def test_rest_population_weight_bitwise(vlbm, vo, alpha):
     lat = vlbm.LatticeParams(alpha=alpha)
     bcs = vlbm.Boundaries(*[vlbm.BcType(b) for b in bc])
     sim = vlbm.BatchSimulation(g, lat, vlbm.GasParams(1.4), bcs, init)
-    r = vo.sim(make_grid(nx, ny, x_max), make_params(gamma=1.4, alpha=alpha, bc=bc), init)
+    r = orc.sim(make_grid(nx, ny, x_max), make_params(gamma=1.4, alpha=alpha, bc=bc), init)
     sim.step(10)
     for _ in range(10):
         r.step(r.suggest_dt())
@@ -535,7 +541,7 @@ def test_rest_population_weight_bitwise(vlbm, vo, alpha):
 
 
 @pytest.mark.parametrize("limiter", [RLMP, FIRST_ORDER])
-def test_graph_replay_matches_direct_launches(vlbm, vo, monkeypatch, limiter):
+def test_graph_replay_matches_direct_launches(vlbm, orc, monkeypatch, limiter):
     """Chunks after a call's first replay as one captured CUDA graph
     (capi.cu march_loop).  With graphs off (VLBM_GRAPHS=0) the same calls --
     run_to over many chunks, two targets, then step(n) -- give identical
@@ -556,7 +562,7 @@ def test_graph_replay_matches_direct_launches(vlbm, vo, monkeypatch, limiter):
         assert_bitwise(out["1"][0][m], out["0"][0][m], f"graph vs direct sample {m}")
     assert list(out["1"][1]) == list(out["0"][1])
     assert out["1"][2] == out["0"][2]
-    r = vo.jet_sim(make_grid(200, 40), make_params(limiter=limiter), make_pert(), 42, 2)
+    r = orc.jet_sim(make_grid(200, 40), make_params(limiter=limiter), make_pert(), 42, 2)
     for target in (0.0003, 0.0005):
         while r.time < target - 1e-12:
             r.step(min(r.suggest_dt(), target - r.time))
@@ -566,7 +572,7 @@ def test_graph_replay_matches_direct_launches(vlbm, vo, monkeypatch, limiter):
     assert_bitwise(out["1"][0][2], r.get(), "graph replay vs oracle")
 
 
-def test_cert_side_stream_matches_in_line(vlbm, vo, monkeypatch):
+def test_cert_side_stream_matches_in_line(vlbm, orc, monkeypatch):
     """k_bisect_cert on its side stream (default) and in line on the main
     stream (VLBM_CERT_SIDE=0) give the same bits at late time, where all
     three bisection kernels have work; both match the oracle."""
@@ -581,7 +587,7 @@ def test_cert_side_stream_matches_in_line(vlbm, vo, monkeypatch):
     for m in range(4):
         assert_bitwise(out["1"][0][m], out["0"][0][m], f"side vs in-line sample {m}")
     assert list(out["1"][1]) == list(out["0"][1])
-    r = vo.jet_sim(make_grid(200, 40), make_params(), make_pert(), 42, 1)
+    r = orc.jet_sim(make_grid(200, 40), make_params(), make_pert(), 42, 1)
     while r.time < 0.0008 - 1e-12:
         r.step(min(r.suggest_dt(), 0.0008 - r.time))
     assert out["1"][1][1] == r.steps
