@@ -224,10 +224,10 @@ int vlbm_batch_kernel_ms(vlbm_batch* b, double* ms);
  * entered, fully certified at the closed-form theta, uncertified, not
  * certifiable, no margin at theta = 0, uncertified vertices at the start
  * (sum), vertex evaluations in the bisections (sum), cells whose diagonal
- * passes at theta = 1, of those vertex-certified, (unused), warps with
- * uncertified lanes, theta = 1 vertex checks deferred from the tile pass to
- * the hard-cell kernel, of those feasible(1), and certificates whose
- * quadratic part dominates.  64-bit counters. */
+ * passes at theta = 1, of those vertex-certified, of those feasible(1),
+ * warps with vertex checks left, and three certificate statistics
+ * (uncertified-but-feasible; of those with the true vertex minimum above
+ * p_FO / 2; of those with the quadratic part dominant). */
 /* Limiter-queue statistics (cumulative since creation): out[0] queue
  * capacity (entries, per sample group), out[1] sample groups (the queues
  * are shared by groups marched one after another on the batch's stream when

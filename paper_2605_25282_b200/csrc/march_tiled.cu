@@ -42,6 +42,13 @@
 #define VLBM_ADV_MINB 4  // resident advance CTAs per SM (register budget)
 #endif
 namespace vlbm_dev {
+#ifndef VLBM_CERT_TRY
+#define VLBM_CERT_TRY 2  // a warp tries the certificate while its hint is at least this
+#endif
+#ifndef VLBM_CERT_PROBE
+#define VLBM_CERT_PROBE 32  // measured: 4 +1.5 %, 8 +1.5 %, 32 ~ 64 ~ 256 (tile pass time)
+#endif
+constexpr int kCertProbe = VLBM_CERT_PROBE;  // steps between re-probes of a warp's certificate
 namespace tiled {
 constexpr int TX = 32, TY = 8, NT = TX * TY;
 constexpr int RX2 = TX + 4, RY2 = TY + 4, NR2 = RX2 * RY2;  // limiter u box (halo 2): 36 x 12
@@ -208,22 +215,9 @@ __device__ __forceinline__ int warp_slot(bool flag, int* counter, int* wbase, in
 // barrier (warps that finish their cells early move on to the next tile).
 // When the queue cannot hold the warp's cells (or is absent) they finish in
 // place.  All lanes of the warp call it.
-// kVertexPending (bit 62 of a hard-queue index): the cell passed the diagonal
-// of feasible(1) and only its 15 vertex floors at theta = 1 are still to be
-// checked (the certificate could not prove them) -- done densely by
-// k_theta_hard instead of by the whole warp here.
-constexpr long long kVertexPending = 1ll << 62;
-
-// rlmp_theta of a queued cell, in one thread (queue overflow paths).
-__device__ __forceinline__ double theta_in_place(const cs& fo, const cs* cf, const RlmpBounds& b,
-                                                 double gm1, bool pending, AuditCtr* audit) {
-  if (pending && vertex_floors_ok(1.0, fo, cf, b, gm1)) return 1.0;
-  return rlmp_theta_hard(fo, cf, b, gm1, audit);
-}
-
 __device__ __forceinline__ void enqueue_hard(const MarchParams& P, bool hard, long long cell,
                                              const cs& fo, const cs* cf, const RlmpBounds& b,
-                                             double gm1, bool pending) {
+                                             double gm1) {
   const unsigned lane = threadIdx.x & 31;
   const unsigned m = __ballot_sync(0xffffffffu, hard);
   if (!m) return;
@@ -251,11 +245,11 @@ __device__ __forceinline__ void enqueue_hard(const MarchParams& P, bool hard, lo
     q[21 * cap] = b.rho_hi;
     q[22 * cap] = b.p_lo;
     q[23 * cap] = b.p_hi;
-    P.hq_idx[slot] = cell | (pending ? kVertexPending : 0ll);
+    P.hq_idx[slot] = cell;
   } else {  // queue full (or absent): finish in place
     if (P.hq && slot < P.hq_cap) P.hq_idx[slot] = -1;
     if (P.qstats && lane == (unsigned)leader) atomicAdd(P.qstats, (unsigned long long)__popc(m));
-    P.theta[cell] = theta_in_place(fo, cf, b, gm1, pending, P.audit);  // rare
+    P.theta[cell] = rlmp_theta_hard(fo, cf, b, gm1, P.audit);  // rare: plain bisection
   }
 }
 
@@ -416,38 +410,57 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_THETA_MINB)
     const int t_next = s_next;
     if (threadIdx.x == 0 && t_next < total) issue(t_next);
 
-    // feasible(1): the diagonal first; then the theta = 1 vertex certificate
-    // (every cell: it proves ~85 % of the diagonal-feasible cells late in the
-    // run).  A cell whose certificate fails is NOT checked here -- one such
-    // lane would make its whole warp run the 15 vertex pressures -- but
-    // queued with kVertexPending and checked densely by k_theta_hard.
+    // feasible(1): the diagonal first; the 15 vertex floors only when the
+    // certificate cannot prove them.  Certificate hint of this warp (warp-
+    // uniform), see MarchParams::cert_hint.
+    unsigned char* hint =
+        P.cert_hint ? P.cert_hint + (long long)t * 8 + (threadIdx.x >> 5) : nullptr;
+    const int h0 = hint ? *hint : 3;
+    const bool try_cert = P.cert1 && (h0 >= VLBM_CERT_TRY || (c->steps % kCertProbe) == 0);
     unsigned aflags = 0;  // audit statistics of this cell (bits = counter indices)
-    bool pending = false;
     if (valid) {
       if (diag_ok(1.0, foC, delta, b, gm1)) {
         double parts[2] = {0.0, 0.0};
-        const bool cert = P.cert1 && vertices_certified_at_one(foC, pfo0, cf, b.rho_floor,
+        const bool cert = try_cert && vertices_certified_at_one(foC, pfo0, cf, b.rho_floor,
                                                                b.p_floor, gm1,
                                                                P.audit ? parts : nullptr);
         need = !cert;
-        if (P.audit) {  // [8] diagonal passed, [9] certified; [0] certificate errors
+#ifdef VLBM_EXP_NOVERTEX  // timing experiment only (WRONG results): the vertex checks' share
+        const bool ok = true;
+#else
+        const bool ok = cert || vertex_floors_ok(1.0, foC, cf, b, gm1);
+#endif
+        if (P.audit) {  // [8] diagonal passed, [9] certified, [10] feasible; [0] certificate errors
           aflags |= 1u << 8;
           if (cert) aflags |= 1u << 9;
+          if (ok) aflags |= 1u << 10;
           if (cert && !vertex_floors_ok(1.0, foC, cf, b, gm1)) aflags |= 1u;
-          if (parts[1] > parts[0]) aflags |= 1u << 14;  // [14] quadratic part dominates
+          if (!cert && ok) {
+            // [12] uncertified but feasible; [13] of those the true vertex
+            // minimum is above p_FO / 2 (bound loose); [14] quadratic part
+            // dominates the bound
+            double pmin = pfo0;
+            for (int mask = 1; mask < 16; ++mask)
+              pmin = smin(pmin, pressure(vertex_at(foC, cf, mask), gm1));
+            aflags |= 1u << 12;
+            if (pmin > 0.5 * pfo0) aflags |= 1u << 13;
+            if (parts[1] > parts[0]) aflags |= 1u << 14;
+          }
         }
-        if (cert)
+        if (ok)
           P.theta[(long long)s * P.plane + (long long)j * P.pitch + i] = 1.0;
         else
-          hard = pending = true;
+          hard = true;
       } else {
         hard = true;
       }
     }
     {
       const unsigned m = __ballot_sync(0xffffffffu, need);
-      if (P.audit && (threadIdx.x & 31) == 0 && m)
-        atomicAdd(P.audit + 11, 1ull);  // [11] warps with uncertified lanes
+      if ((threadIdx.x & 31) == 0) {
+        if (hint && try_cert) *hint = (unsigned char)(m == 0 ? min(h0 + 1, 3) : max(h0 - 1, 0));
+        if (P.audit && m) atomicAdd(P.audit + 11, 1ull);  // [11] warps with vertex checks left
+      }
       if (P.audit) {  // warp-aggregated: one atomic per counter and warp
         for (int k = 0; k < 15; ++k) {
           const unsigned mk = __ballot_sync(0xffffffffu, (aflags >> k) & 1u);
@@ -456,7 +469,7 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_THETA_MINB)
       }
     }
     const long long cell = (long long)s * P.plane + (long long)j * P.pitch + i;
-    enqueue_hard(P, hard, cell, foC, cf, b, gm1, pending);
+    enqueue_hard(P, hard, cell, foC, cf, b, gm1);
     t = t_next;
   }
 }
@@ -536,28 +549,12 @@ __global__ void __launch_bounds__(256, 2) k_theta_hard(MarchParams P) {
     RlmpBounds b;
     HardStage h;
     mbar_wait(&bar, it & 1);
-    bool pending = false;
     if (slot < n) {
       idx = HI[threadIdx.x];
       load_hard_staged(P, H, threadIdx.x, fo, cf, b);
-      if (idx >= 0) {
-        pending = (idx & kVertexPending) != 0;
-        idx &= ~kVertexPending;
-      }
     }
     __syncthreads();  // the buffer is free: next chunk
     if (threadIdx.x == 0 && chunk + (int)gridDim.x < nchunks) issue(chunk + gridDim.x);
-    if (pending) {  // the rest of feasible(1): its 15 vertex floors (diagonal passed)
-      const bool ok = vertex_floors_ok(1.0, fo, cf, b, gm1);
-      if (P.audit) {
-        atomicAdd(P.audit + 12, 1ull);  // [12] vertex checks deferred from the tile pass
-        if (ok) atomicAdd(P.audit + 13, 1ull);  // [13] of those feasible at 1
-      }
-      if (ok) {
-        P.theta[idx] = 1.0;
-        idx = -1;
-      }
-    }
     if (idx >= 0) {
       delta = add(add(cf[0], cf[1]), add(cf[2], cf[3]));
       if (!(finite4(fo) && finite4(cf[0]) && finite4(cf[1]) && finite4(cf[2]) && finite4(cf[3]) &&

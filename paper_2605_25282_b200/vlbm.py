@@ -413,8 +413,8 @@ class BatchSimulation:
         return dict(mismatches=n[0], bisections=n[1], certified_at_thc=n[2], uncertified=n[3],
                     not_certifiable=n[4], no_margin_at_0=n[5], unc_vertices_start=n[6],
                     vertex_evals=n[7], diag_ok_at_1=n[8], vertex_certified_at_1=n[9],
-                    warps_with_uncertified=n[11], deferred_vertex_checks=n[12],
-                    deferred_feasible_at_1=n[13], cert_quad_dominant=n[14])
+                    feasible_at_1=n[10], warps_with_vertex_checks=n[11],
+                    unc_feasible=n[12], unc_feasible_loose=n[13], unc_feasible_quad=n[14])
 
     def audit_mismatches(self) -> int:
         return self.audit_counters()["mismatches"]

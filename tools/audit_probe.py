@@ -21,6 +21,6 @@ for t in (0.0002, 0.0005, 0.001, 0.0015, 0.002, 0.0025):
     per = lambda k: d[k] / n
     print(f"t={t}: mismatches={c['mismatches']} per sample-step of {g.cells()} cells: "
           f"diag_ok={per('diag_ok_at_1'):.0f} certified={per('vertex_certified_at_1'):.0f} "
-          f"deferred={per('deferred_vertex_checks'):.0f} bisections={per('bisections'):.0f} "
+          f"feasible={per('feasible_at_1'):.0f} bisections={per('bisections'):.0f} "
           f"uncertified={per('uncertified'):.0f} unc_vertices_start={per('unc_vertices_start'):.0f} "
           f"vertex_evals={per('vertex_evals'):.0f}", flush=True)

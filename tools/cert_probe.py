@@ -18,5 +18,5 @@ sim.step(N)
 a = sim.audit_counters()
 cells = 64 * N * g.cells()
 print(json.dumps({"T": T, "steps": N, **{k: a[k] / cells for k in a if k != "mismatches"},
-                  "warps_with_uncertified_per_warp": a["warps_with_uncertified"] / (cells / 32),
+                  "warps_with_vertex_checks_per_warp": a["warps_with_vertex_checks"] / (cells / 32),
                   "mismatches": a["mismatches"]}))
