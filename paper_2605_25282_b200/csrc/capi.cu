@@ -198,7 +198,7 @@ int alloc_batch(const vlbm_grid* g, const vlbm_params* p, int S, int device, vlb
   P.replay = 1;
   if (const char* e = getenv("VLBM_REPLAY")) P.replay = atoi(e) != 0;
   {
-    const size_t n = (size_t)S * vlbm_impl::theta_tiles(P.nx, P.ny) * 8;
+    const size_t n = (size_t)S * vlbm_impl::theta_tiles(P.nx, P.ny) * VLBM_THETA_TY;
     if (n / 8 > (size_t)INT_MAX) rc = set_error(VLBM_E_INVALID, "too many tiles for one batch");
     // VLBM_CERT_HINT=0 (A/B switch): no hints, every warp tries the certificate
     const char* e = getenv("VLBM_CERT_HINT");
@@ -258,7 +258,8 @@ int alloc_batch(const vlbm_grid* g, const vlbm_params* p, int S, int device, vlb
     Q.inlet = P.inlet + (size_t)s0 * P.ny * 4;
     Q.n_active = b->d_active_g + g;
     Q.cert_hint =
-        P.cert_hint ? P.cert_hint + (size_t)s0 * vlbm_impl::theta_tiles(P.nx, P.ny) * 8 : nullptr;
+        P.cert_hint ? P.cert_hint + (size_t)s0 * vlbm_impl::theta_tiles(P.nx, P.ny) * VLBM_THETA_TY
+                    : nullptr;
     Q.persist_ctas = std::max(1, sms * vlbm_impl::theta_ctas_per_sm() / (b->serial ? 1 : G));
     cudaStream_t sg = b->stream;
     if (g > 0 && !b->serial) chk(cudaStreamCreateWithFlags(&sg, cudaStreamNonBlocking), "stream g");

@@ -51,8 +51,14 @@ cudaError_t launch_theta_tiled(const vlbm_dev::MarchParams& P, cudaStream_t st);
 cudaError_t launch_theta_hard(const vlbm_dev::MarchParams& P, cudaStream_t st);
 // Resident k_theta_tiled CTAs per SM (occupancy of the persistent tile pass).
 int theta_ctas_per_sm();
-// Tiles of k_theta_tiled's grid (32 x 8 cells each) per sample.
-inline int theta_tiles(int nx, int ny) { return ((nx + 31) / 32) * ((ny + 7) / 8); }
+// Tiles of k_theta_tiled's grid (32 x VLBM_THETA_TY cells, one warp per row)
+// per sample.
+#ifndef VLBM_THETA_TY
+#define VLBM_THETA_TY 8
+#endif
+inline int theta_tiles(int nx, int ny) {
+  return ((nx + 31) / 32) * ((ny + VLBM_THETA_TY - 1) / VLBM_THETA_TY);
+}
 cudaError_t launch_advance_tiled(const vlbm_dev::MarchParams& P, int mode, double const_theta,
                                  cudaStream_t st);
 cudaError_t launch_set_budget(const vlbm_dev::MarchParams& P, long long budget,

@@ -50,17 +50,20 @@ namespace vlbm_dev {
 #endif
 constexpr int kCertProbe = VLBM_CERT_PROBE;  // steps between re-probes of a warp's certificate
 namespace tiled {
-constexpr int TX = 32, TY = 8, NT = TX * TY;
-constexpr int RX2 = TX + 4, RY2 = TY + 4, NR2 = RX2 * RY2;  // limiter u box (halo 2): 36 x 12
-constexpr int RX1 = TX + 2, RY1 = TY + 2, NR1 = RX1 * RY1;  // halo-1 box: 34 x 10
+constexpr int TX = 32, TY = 8, NT = TX * TY;  // advance tile
+// limiter tile pass: TX x TYT cells, one warp per row
+constexpr int TYT = VLBM_THETA_TY, NTT = TX * TYT;
+constexpr int RX2 = TX + 4, RY2 = TYT + 4, NR2 = RX2 * RY2;  // limiter u box (halo 2): 36 x 12
+constexpr int RX1 = TX + 2, RY1 = TYT + 2, NR1 = RX1 * RY1;  // halo-1 box: 34 x 10
 constexpr int FX = RX1, NF = NR1;                           // u_FO ring region
+constexpr int AYT = TYT + 2, NAT = (TX + 4) * AYT;          // limiter population box: 36 x 10
 // TMA boxes start at an even x (16-byte aligned for 8-byte elements; an odd
 // origin faults): the halo-1 boxes are loaded from x0-2, 36 wide.
 constexpr int AX = TX + 4, AY = TY + 2, NA = AX * AY;        // 36 x 10
 constexpr int kStagedTheta = 13;  // u(4) [TMA], inv2a*f(4), inv2a*g(4), p
 // limiter smem: R [13][NR2] | RF [2][NF] | pad | SP [16][NA] (TMA, 128-B aligned)
 constexpr int kThetaSP = ((kStagedTheta * NR2 + 2 * NF) + 15) / 16 * 16;
-constexpr int kThetaSPn = VLBM_THETA_GPOP ? 0 : 16 * NA;
+constexpr int kThetaSPn = VLBM_THETA_GPOP ? 0 : 16 * NAT;
 constexpr size_t kThetaSmem = sizeof(double) * (kThetaSP + kThetaSPn);
 constexpr unsigned kThetaTx = sizeof(double) * (4 * NR2 + kThetaSPn);
 // advance smem: R [4][NA] (TMA: u) | F [8][NA] (inv2a f, inv2a g); the
@@ -260,7 +263,7 @@ __device__ __forceinline__ void enqueue_hard(const MarchParams& P, bool hard, lo
 // tile's staged data is read only until its cells hold u_FO, c_f and the
 // bounds in registers; then the CTA issues the NEXT tile's TMA into the same
 // buffers, so the load overlaps this tile's feasibility work.
-__global__ void __launch_bounds__(tiled::NT, VLBM_THETA_MINB)
+__global__ void __launch_bounds__(tiled::NTT, VLBM_THETA_MINB)
     k_theta_tiled(MarchParams P, const __grid_constant__ CUtensorMap tmu0,
                   const __grid_constant__ CUtensorMap tmu1, const __grid_constant__ CUtensorMap tmp0,
                   const __grid_constant__ CUtensorMap tmp1) {
@@ -270,8 +273,8 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_THETA_MINB)
   __shared__ int s_next;
   double* R = sm;                    // u [4][NR2] by TMA, then inv2a f/g, p: [9][NR2]
   double* RF = R + kStagedTheta * NR2;  // rfo[NF], pfo[NF]
-  double* SP = sm + kThetaSP;        // populations [16][NA] by TMA
-  const int tiles_x = (P.nx + TX - 1) / TX, tiles_y = (P.ny + TY - 1) / TY;
+  double* SP = sm + kThetaSP;        // populations [16][NAT] by TMA
+  const int tiles_x = (P.nx + TX - 1) / TX, tiles_y = (P.ny + TYT - 1) / TYT;
   const int per_sample = tiles_x * tiles_y;
   const int total = P.S * per_sample;  // < 2^31 tiles (host-checked)
   const double gm1 = P.gm1, w = P.w, al = P.alpha;
@@ -296,7 +299,7 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_THETA_MINB)
   };
   auto issue = [&](int t) {  // thread 0: the tile's TMA loads
     const int s = t / per_sample, r = t - s * per_sample;
-    const int x0 = (r % tiles_x) * TX, y0 = (r / tiles_x) * TY;
+    const int x0 = (r % tiles_x) * TX, y0 = (r / tiles_x) * TYT;
     const int parity = P.ctl[s].parity;
     mbar_expect_tx(&bar, kThetaTx);
     tma_load_4d(R, parity ? &tmu1 : &tmu0, &bar, x0 - 2, y0 - 2, 0, s);
@@ -309,7 +312,7 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_THETA_MINB)
   if (threadIdx.x == 0) issue(t);
   for (unsigned it = 0; t < total; ++it) {
     const int s = t / per_sample, r = t - s * per_sample;
-    const int x0 = (r % tiles_x) * TX, y0 = (r / tiles_x) * TY;
+    const int x0 = (r % tiles_x) * TX, y0 = (r / tiles_x) * TYT;
     const SampleCtl* c = P.ctl + s;
     const int parity = c->parity;
     const double* src = state_src(P, s, parity);
@@ -318,13 +321,13 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_THETA_MINB)
     int tn_claim = 0;
     if (threadIdx.x == 0) tn_claim = claim_start(t);
     mbar_wait(&bar, it & 1u);
-    if (!(x0 >= 2 && x0 + TX + 2 <= P.nx && y0 >= 2 && y0 + TY + 2 <= P.ny)) {
+    if (!(x0 >= 2 && x0 + TX + 2 <= P.nx && y0 >= 2 && y0 + TYT + 2 <= P.ny)) {
       patch_box<false>(P, src, rows, R, RX2, RY2, x0 - 2, y0 - 2, inv2a);
-      if (!VLBM_THETA_GPOP) patch_box<true>(P, src, rows, SP, AX, AY, x0 - 2, y0 - 1, inv2a);
+      if (!VLBM_THETA_GPOP) patch_box<true>(P, src, rows, SP, AX, AYT, x0 - 2, y0 - 1, inv2a);
       __syncthreads();
     }
     double* F = R + 4 * NR2;
-    for (int q = threadIdx.x; q < NR2; q += NT) flux_cell(R, NR2, F, NR2, q, inv2a, gm1, true);
+    for (int q = threadIdx.x; q < NR2; q += NTT) flux_cell(R, NR2, F, NR2, q, inv2a, gm1, true);
     __syncthreads();
 
     // First-order candidates (compute_candidates, solver.hpp:301-316) on the
@@ -341,17 +344,17 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_THETA_MINB)
     cs foC = ufo_at(tx, ty);
     RF[fq(tx, ty)] = foC.r;
     RF[NF + fq(tx, ty)] = pressure(foC, gm1);
-    if (threadIdx.x < 2 * TX + 2 * TY) {
+    if (threadIdx.x < 2 * TX + 2 * TYT) {
       const int q = threadIdx.x;
       int x, y;
       if (q < TX) {
         x = q, y = -1;
       } else if (q < 2 * TX) {
-        x = q - TX, y = TY;
-      } else if (q < 2 * TX + TY) {
+        x = q - TX, y = TYT;
+      } else if (q < 2 * TX + TYT) {
         x = -1, y = q - 2 * TX;
       } else {
-        x = TX, y = q - 2 * TX - TY;
+        x = TX, y = q - 2 * TX - TYT;
       }
       const cs fo = ufo_at(x, y);
       RF[fq(x, y)] = fo.r;
@@ -375,7 +378,7 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_THETA_MINB)
             return load_plane4(src + (4 + 4 * k) * P.plane, P.plane, (long long)jj * P.pitch + ii);
           return load_pop(P, src, rows, k, ii, jj, inv2a);
         }
-        return plane4(SP + 4 * k * NA, NA, (y + 1) * AX + (x + 2));
+        return plane4(SP + 4 * k * NAT, NAT, (y + 1) * AX + (x + 2));
       };
       const int qc = rq(tx, ty);
       cf[0] = sub(sub(M(rq(tx - 1, ty), 0), pop(0, tx - 1, ty)), sub(M(qc, 1), pop(1, tx, ty)));
@@ -414,7 +417,7 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_THETA_MINB)
     // certificate cannot prove them.  Certificate hint of this warp (warp-
     // uniform), see MarchParams::cert_hint.
     unsigned char* hint =
-        P.cert_hint ? P.cert_hint + (long long)t * 8 + (threadIdx.x >> 5) : nullptr;
+        P.cert_hint ? P.cert_hint + (long long)t * TYT + (threadIdx.x >> 5) : nullptr;
     const int h0 = hint ? *hint : 3;
     const bool try_cert = P.cert1 && (h0 >= VLBM_CERT_TRY || (c->steps % kCertProbe) == 0);
     unsigned aflags = 0;  // audit statistics of this cell (bits = counter indices)
@@ -892,7 +895,7 @@ static cudaError_t smem_attrs() {
   return r;
 }
 
-static_assert(tiled::TX == 32 && tiled::TY == 8 && tiled::NT == 256, "theta_tiles() layout");
+static_assert(tiled::TX == 32 && tiled::TYT == VLBM_THETA_TY, "theta_tiles() layout");
 // grid: (tile x, tile y, sample)
 static dim3 tiled_grid(const MarchParams& P) {
   return dim3((P.nx + tiled::TX - 1) / tiled::TX, (P.ny + tiled::TY - 1) / tiled::TY, P.S);
@@ -922,7 +925,7 @@ int encode_tensor_maps(MarchParams& P) {
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   const cuuint32_t box_adv[4] = {tiled::AX, tiled::AY, 4, 1};
   const cuuint32_t box_thu[4] = {tiled::RX2, tiled::RY2, 4, 1};
-  const cuuint32_t box_thp[4] = {tiled::AX, tiled::AY, 16, 1};
+  const cuuint32_t box_thp[4] = {tiled::AX, tiled::AYT, 16, 1};
   for (int b = 0; b < 2; ++b) {
     void* base = b ? P.buf1 : P.buf0;
     CUresult r = encode(&P.tm_adv[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, base, dims, strides,
@@ -947,7 +950,7 @@ cudaError_t launch_theta_tiled(const MarchParams& P, cudaStream_t st) {
   // persistent: the resident CTAs of this sample group's share of the GPU
   const long long tiles = (long long)P.S * theta_tiles(P.nx, P.ny);
   const int g = (int)(tiles < P.persist_ctas ? tiles : P.persist_ctas);
-  k_theta_tiled<<<g, tiled::NT, tiled::kThetaSmem, st>>>(P, P.tm_thu[0], P.tm_thu[1],
+  k_theta_tiled<<<g, tiled::NTT, tiled::kThetaSmem, st>>>(P, P.tm_thu[0], P.tm_thu[1],
                                                           P.tm_thp[0], P.tm_thp[1]);
   return cudaGetLastError();
 }
@@ -955,7 +958,7 @@ cudaError_t launch_theta_tiled(const MarchParams& P, cudaStream_t st) {
 int theta_ctas_per_sm() {
   if (smem_attrs() != cudaSuccess) return 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_theta_tiled, tiled::NT,
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_theta_tiled, tiled::NTT,
                                                     tiled::kThetaSmem) != cudaSuccess)
     return 1;
   return n > 0 ? n : 1;
