@@ -115,12 +115,17 @@ class ClockSampler:
 def fp64_profile():
     """Per-launch DRAM bytes of the advance and limiter kernels and the
     limiter's FP64 instructions per cell, from the committed ncu capture
-    (profiles/r1_roofline_inputs.json: tools/profile_r1.sh + summarize_profiles.py)."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r1_roofline_inputs.json")) as f:
-            return json.load(f)
-    except Exception:
-        return None
+    (profiles/r<N>_roofline_inputs.json, the latest round's:
+    tools/profile_round.sh + summarize_profiles.py)."""
+    for tag in ("r2", "r1"):
+        try:
+            with open(os.path.join(ROOT, "profiles", f"{tag}_roofline_inputs.json")) as f:
+                d = json.load(f)
+            d["source"] = f"profiles/{tag}_kernels.csv"
+            return d
+        except Exception:
+            continue
+    return None
 
 
 def dist_env():
@@ -671,7 +676,7 @@ def main():
                     "peak_source": src, "bytes_per_cell": BYTES_PER_UPDATE,
                     "cells_per_launch": cells_per_launch, "launch_ms": kern["ms_advance"],
                     "note": "per-launch times: CUDA events around each launch in the timed "
-                            "region; traffic from profiles/r1_kernels.csv (ncu --set full)"}
+                            f"region; traffic from {prof.get('source', 'profiles/')} (ncu --set full)"}
             # The limiter's tile pass, the longest kernel of the step: FP64-bound.
             t_tiles = kern["ms_theta_tiles"] * 1e-3
             lim_gbs = THETA_BYTES_PER_CELL * cells_per_launch / t_tiles / 1e9

@@ -125,7 +125,6 @@ void free_batch(vlbm_batch* b) {
   cudaFree(b->d_face_tx);
   cudaFree(b->d_face_ty);
   cudaFree(b->P.audit);
-  cudaFree(b->P.cert_hint);
   if (b->h_active) cudaFreeHost(b->h_active);
   for (cudaEvent_t e : b->ev) cudaEventDestroy(e);
   if (b->stream) cudaStreamDestroy(b->stream);
@@ -197,16 +196,8 @@ int alloc_batch(const vlbm_grid* g, const vlbm_params* p, int S, int device, vlb
   if (const char* e = getenv("VLBM_CERT1")) P.cert1 = atoi(e) != 0;
   P.replay = 1;
   if (const char* e = getenv("VLBM_REPLAY")) P.replay = atoi(e) != 0;
-  {
-    const size_t n = (size_t)S * vlbm_impl::theta_tiles(P.nx, P.ny) * VLBM_THETA_TY;
-    if (n / 8 > (size_t)INT_MAX) rc = set_error(VLBM_E_INVALID, "too many tiles for one batch");
-    // VLBM_CERT_HINT=0 (A/B switch): no hints, every warp tries the certificate
-    const char* e = getenv("VLBM_CERT_HINT");
-    if (!e || atoi(e) != 0) {
-      chk(cudaMalloc(&P.cert_hint, n), "malloc cert_hint");
-      if (rc == VLBM_OK) chk(cudaMemset(P.cert_hint, 3, n), "memset cert_hint");
-    }
-  }
+  if ((size_t)S * vlbm_impl::theta_tiles(P.nx, P.ny) > (size_t)INT_MAX)
+    rc = set_error(VLBM_E_INVALID, "too many tiles for one batch");
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   if (const char* e = getenv("VLBM_GRAPHS")) b->graphs = atoi(e) != 0;
@@ -257,9 +248,6 @@ int alloc_batch(const vlbm_grid* g, const vlbm_params* p, int S, int device, vlb
     Q.theta = P.theta + (size_t)s0 * P.plane;
     Q.inlet = P.inlet + (size_t)s0 * P.ny * 4;
     Q.n_active = b->d_active_g + g;
-    Q.cert_hint =
-        P.cert_hint ? P.cert_hint + (size_t)s0 * vlbm_impl::theta_tiles(P.nx, P.ny) * VLBM_THETA_TY
-                    : nullptr;
     Q.persist_ctas = std::max(1, sms * vlbm_impl::theta_ctas_per_sm() / (b->serial ? 1 : G));
     cudaStream_t sg = b->stream;
     if (g > 0 && !b->serial) chk(cudaStreamCreateWithFlags(&sg, cudaStreamNonBlocking), "stream g");

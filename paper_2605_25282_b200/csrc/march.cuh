@@ -84,14 +84,10 @@ struct MarchParams {
   // summed over passes, [3] passes.  Updated by the limiter kernels / k_sched.
   unsigned long long* qstats;
   AuditCtr* audit;    // optional: disagreements of the certified bisection (must stay 0)
-  int cert1;     // use the theta = 1 vertex certificate (A/B switch VLBM_CERT1, default on)
+  int cert1;     // decide the theta = 1 vertex floors by the quadratic form (rlmp.cuh;
+                 // A/B switch VLBM_CERT1, default on; 0: always the exact checks)
   int replay;    // k_bisect_unc replays its bisections from certified classifications
                  // (rlmp_replay.cuh; A/B switch VLBM_REPLAY, default on)
-  // Per (sample, tile, warp) hint of the limiter: a 2-bit saturating count of
-  // the certificate proving every lane's vertex floors (+1) or not (-1) at its
-  // attempts; tried while >= 2, else re-probed every kCertProbe-th step.
-  // k_theta_tiled's grid, 8 warps per tile; starts at 3.
-  unsigned char* cert_hint;
   int persist_ctas;  // grid of the persistent limiter tile pass (this group's share of the GPU)
   // TMA tensor maps [x, y, plane, sample] of buffer 0/1 with the tile boxes of
   // the advance (34x10x20), the limiter's u (36x12x4) and populations (34x10x16).

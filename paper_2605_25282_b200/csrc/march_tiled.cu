@@ -42,13 +42,6 @@
 #define VLBM_ADV_MINB 4  // resident advance CTAs per SM (register budget)
 #endif
 namespace vlbm_dev {
-#ifndef VLBM_CERT_TRY
-#define VLBM_CERT_TRY 2  // a warp tries the certificate while its hint is at least this
-#endif
-#ifndef VLBM_CERT_PROBE
-#define VLBM_CERT_PROBE 32  // measured: 4 +1.5 %, 8 +1.5 %, 32 ~ 64 ~ 256 (tile pass time)
-#endif
-constexpr int kCertProbe = VLBM_CERT_PROBE;  // steps between re-probes of a warp's certificate
 namespace tiled {
 constexpr int TX = 32, TY = 8, NT = TX * TY;  // advance tile
 // limiter tile pass: TX x TYT cells, one warp per row
@@ -278,6 +271,7 @@ __global__ void __launch_bounds__(tiled::NTT, VLBM_THETA_MINB)
   const int per_sample = tiles_x * tiles_y;
   const int total = P.S * per_sample;  // < 2^31 tiles (host-checked)
   const double gm1 = P.gm1, w = P.w, al = P.alpha;
+  const double igm1 = 1.0 / gm1;
   auto next_active = [&](int t) {
     while (t < total && !P.ctl[t / per_sample].active) t += gridDim.x;
     return t;
@@ -368,8 +362,7 @@ __global__ void __launch_bounds__(tiled::NTT, VLBM_THETA_MINB)
     const bool valid = i < P.nx && j < P.ny;
     cs cf[4], delta;
     RlmpBounds b;
-    double pfo0 = 0.0;
-    bool hard = false, need = false;
+    bool hard = false;
     if (valid) {
       auto pop = [&](int k, int x, int y) {
         if (VLBM_THETA_GPOP) {
@@ -403,7 +396,6 @@ __global__ void __launch_bounds__(tiled::NTT, VLBM_THETA_MINB)
         st.pprev[n] = F[8 * NR2 + rpts[n]];
       }
       b = rlmp_bounds(st, P.kappa, P.rho_floor_coef, P.p_floor_coef);
-      pfo0 = st.pfo[0];
       delta = add(add(cf[0], cf[1]), add(cf[2], cf[3]));
     }
     // The staged buffers are free: prefetch the next tile (claimed before the
@@ -413,42 +405,25 @@ __global__ void __launch_bounds__(tiled::NTT, VLBM_THETA_MINB)
     const int t_next = s_next;
     if (threadIdx.x == 0 && t_next < total) issue(t_next);
 
-    // feasible(1): the diagonal first; the 15 vertex floors only when the
-    // certificate cannot prove them.  Certificate hint of this warp (warp-
-    // uniform), see MarchParams::cert_hint.
-    unsigned char* hint =
-        P.cert_hint ? P.cert_hint + (long long)t * TYT + (threadIdx.x >> 5) : nullptr;
-    const int h0 = hint ? *hint : 3;
-    const bool try_cert = P.cert1 && (h0 >= VLBM_CERT_TRY || (c->steps % kCertProbe) == 0);
+    // feasible(1): the diagonal first; then the 15 vertex floors decided by
+    // the quadratic form (rlmp.cuh::vertex_floors_quadform: no pressure
+    // divisions), evaluated exactly only for the few cells it leaves open.
     unsigned aflags = 0;  // audit statistics of this cell (bits = counter indices)
     if (valid) {
       if (diag_ok(1.0, foC, delta, b, gm1)) {
-        double parts[2] = {0.0, 0.0};
-        const bool cert = try_cert && vertices_certified_at_one(foC, pfo0, cf, b.rho_floor,
-                                                               b.p_floor, gm1,
-                                                               P.audit ? parts : nullptr);
-        need = !cert;
+        const int q = P.cert1 ? vertex_floors_quadform(foC, cf, b.rho_floor, b.p_floor, gm1, igm1)
+                              : -1;
 #ifdef VLBM_EXP_NOVERTEX  // timing experiment only (WRONG results): the vertex checks' share
         const bool ok = true;
 #else
-        const bool ok = cert || vertex_floors_ok(1.0, foC, cf, b, gm1);
+        const bool ok = q > 0 || (q < 0 && vertex_floors_ok(1.0, foC, cf, b, gm1));
 #endif
-        if (P.audit) {  // [8] diagonal passed, [9] certified, [10] feasible; [0] certificate errors
+        if (P.audit) {  // [8] diagonal passed, [9] decided by the form, [10] feasible; [0] its errors
           aflags |= 1u << 8;
-          if (cert) aflags |= 1u << 9;
+          if (q >= 0) aflags |= 1u << 9;
           if (ok) aflags |= 1u << 10;
-          if (cert && !vertex_floors_ok(1.0, foC, cf, b, gm1)) aflags |= 1u;
-          if (!cert && ok) {
-            // [12] uncertified but feasible; [13] of those the true vertex
-            // minimum is above p_FO / 2 (bound loose); [14] quadratic part
-            // dominates the bound
-            double pmin = pfo0;
-            for (int mask = 1; mask < 16; ++mask)
-              pmin = smin(pmin, pressure(vertex_at(foC, cf, mask), gm1));
-            aflags |= 1u << 12;
-            if (pmin > 0.5 * pfo0) aflags |= 1u << 13;
-            if (parts[1] > parts[0]) aflags |= 1u << 14;
-          }
+          if (q >= 0 && (q > 0) != vertex_floors_ok(1.0, foC, cf, b, gm1)) aflags |= 1u;
+          if (q < 0) aflags |= 1u << 12;  // [12] left open: exact vertex checks
         }
         if (ok)
           P.theta[(long long)s * P.plane + (long long)j * P.pitch + i] = 1.0;
@@ -458,17 +433,10 @@ __global__ void __launch_bounds__(tiled::NTT, VLBM_THETA_MINB)
         hard = true;
       }
     }
-    {
-      const unsigned m = __ballot_sync(0xffffffffu, need);
-      if ((threadIdx.x & 31) == 0) {
-        if (hint && try_cert) *hint = (unsigned char)(m == 0 ? min(h0 + 1, 3) : max(h0 - 1, 0));
-        if (P.audit && m) atomicAdd(P.audit + 11, 1ull);  // [11] warps with vertex checks left
-      }
-      if (P.audit) {  // warp-aggregated: one atomic per counter and warp
-        for (int k = 0; k < 15; ++k) {
-          const unsigned mk = __ballot_sync(0xffffffffu, (aflags >> k) & 1u);
-          if ((threadIdx.x & 31) == 0 && mk) atomicAdd(P.audit + k, (AuditCtr)__popc(mk));
-        }
+    if (P.audit) {  // warp-aggregated: one atomic per counter and warp
+      for (int k = 0; k < 15; ++k) {
+        const unsigned mk = __ballot_sync(0xffffffffu, (aflags >> k) & 1u);
+        if ((threadIdx.x & 31) == 0 && mk) atomicAdd(P.audit + k, (AuditCtr)__popc(mk));
       }
     }
     const long long cell = (long long)s * P.plane + (long long)j * P.pitch + i;

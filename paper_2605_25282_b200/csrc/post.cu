@@ -27,8 +27,11 @@
 
 #include "internal.h"
 
-#ifndef VLBM_W1_MERGE
-#define VLBM_W1_MERGE 1  // W1 sort: per-lane sort + merge-path levels (0: bitonic network)
+#ifndef VLBM_W1_SORT
+// W1 per-cell sort: 2 = 32-bit quantised keys + index through the bitonic
+// network, exact order restored among equal quantised keys (default);
+// 1 = per-lane sort + merge-path levels on 64-bit keys; 0 = 64-bit bitonic network
+#define VLBM_W1_SORT 1
 #endif
 
 namespace vlbm_dev {
@@ -186,28 +189,25 @@ __device__ __forceinline__ double dval(unsigned long long k) {
 // logic: 3 instructions per element for an in-register stage, 7 for a
 // cross-lane one (2 shuffles, 64-bit compare, xor, 2 selects).  Element
 // e = lane*R + r.
-template <int R>
-__device__ __forceinline__ void warp_sort_asc(unsigned long long (&v)[R], int lane) {
-  auto cas = [](unsigned long long& lo, unsigned long long& hi) {
-    const bool lt = hi < lo;
-    const unsigned long long a = lo, b = hi;
-    lo = lt ? b : a;
-    hi = lt ? a : b;
+template <int R, typename T>
+__device__ __forceinline__ void warp_sort_asc(T (&v)[R], int lane) {
+  auto cas = [](T& lo, T& hi) {
+    const T a = lo, b = hi;
+    lo = min(a, b);
+    hi = max(a, b);
   };
   // cross-lane step: partner lane ^ m, partner register pr(r); this lane is the
   // upper side iff (lane & topbit) != 0
   auto xlane = [&](int m, int topbit, bool reverse) {
     const bool upper = (lane & topbit) != 0;
-    auto upd = [&](unsigned long long& x, unsigned long long o) {
-      x = ((o < x) != upper) ? o : x;  // lower: min, upper: max
-    };
+    auto upd = [&](T& x, T o) { x = upper ? max(x, o) : min(x, o); };
     if (reverse) {  // partner register R-1-r: exchange mirrored pairs together
 #pragma unroll
       for (int r = 0; r < (R + 1) / 2; ++r) {
         const int q = R - 1 - r;
-        const unsigned long long o1 = __shfl_xor_sync(kFull, v[q], m);
+        const T o1 = __shfl_xor_sync(kFull, v[q], m);
         if (q != r) {
-          const unsigned long long o2 = __shfl_xor_sync(kFull, v[r], m);
+          const T o2 = __shfl_xor_sync(kFull, v[r], m);
           upd(v[q], o2);
         }
         upd(v[r], o1);
@@ -336,7 +336,7 @@ __device__ __forceinline__ double w1_cell(int M, int lane, double* ca, const dou
       const int m = r * 32 + lane;  // load slot order is free: sorting is order-free
       k[r] = m < M ? dkey(col[m]) : ~0ull;
     }
-#if VLBM_W1_MERGE
+#if VLBM_W1_SORT == 1
     __syncwarp();  // the column is free once every lane holds its keys
     warp_merge_sort<R>(k, lane,
                        reinterpret_cast<unsigned long long*>(const_cast<double*>(col)));

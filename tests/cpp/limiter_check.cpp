@@ -6,7 +6,8 @@
 //   queued    rlmp_hard_stage + bisect_certified / bisect_uncertified (replay off)
 //   replay    rlmp_hard_stage + bisect_replay with at most kReplayInline exact
 //             steps, the rest resumed by bisect_uncertified (k_bisect_tail)
-// and the theta = 1 vertex certificate must never certify an infeasible cell.
+// and the theta = 1 quadratic-form decision of the vertex floors
+// (vertex_floors_quadform) must never contradict the exact checks.
 // The audit counters (a re-run of the full feasible() at every step) must
 // stay zero.  Output: one JSON line of counts.
 // usage: limiter_check records.bin   (27 doubles per cell, see vlbm_oracle.h)
@@ -47,8 +48,9 @@ int main(int argc, char** argv) {
   if (!f) return 2;
   const double gm1 = std::atof(argv[2]) - 1.0;
   double r[27];
-  long cells = 0, at_one = 0, cert = 0, cert_bad = 0, hard = 0, bisect = 0, stopped = 0;
+  long cells = 0, at_one = 0, hard = 0, bisect = 0, stopped = 0;
   long bad_plain = 0, bad_queued = 0, bad_replay = 0, margin_bad = 0;
+  long quad_pass = 0, quad_fail = 0, quad_open = 0, quad_bad = 0;
   unsigned long long audit[16] = {0};
   while (std::fread(r, sizeof r, 1, f) == 1) {
     ++cells;
@@ -60,10 +62,12 @@ int main(int argc, char** argv) {
     const cs delta = add(add(cf[0], cf[1]), add(cf[2], cf[3]));
     if (diag_ok(1.0, fo, delta, b, gm1)) {
       const bool ok = vertex_floors_ok(1.0, fo, cf, b, gm1);
-      const bool c = vertices_certified_at_one(fo, pressure(fo, gm1), cf, b.rho_floor, b.p_floor,
-                                               gm1);
-      cert += c;
-      cert_bad += c && !ok;
+      // the quadratic-form decision of the same 15 checks: never contradicts them
+      const int q = vertex_floors_quadform(fo, cf, b.rho_floor, b.p_floor, gm1, 1.0 / gm1);
+      quad_pass += q == 1;
+      quad_fail += q == 0;
+      quad_open += q < 0;
+      quad_bad += (q == 1 && !ok) || (q == 0 && ok);
       if (ok) {
         ++at_one;
         bad_plain += !same(want, 1.0);
@@ -127,11 +131,13 @@ int main(int argc, char** argv) {
     hyp_bad += !same(want, got);
   }
   std::printf(
-      "{\"cells\": %ld, \"theta_one\": %ld, \"certified_at_one\": %ld, \"certificate_errors\": %ld, "
+      "{\"cells\": %ld, \"theta_one\": %ld, "
       "\"hard\": %ld, \"bisections\": %ld, \"replay_stopped\": %ld, \"mismatch_plain\": %ld, "
       "\"mismatch_queued\": %ld, \"mismatch_replay\": %ld, \"audit_errors\": %llu, "
-      "\"margin_errors\": %ld, \"hypot_checks\": %ld, \"hypot_errors\": %ld}\n",
-      cells, at_one, cert, cert_bad, hard, bisect, stopped, bad_plain, bad_queued, bad_replay,
-      audit[0], margin_bad, hyp_n, hyp_bad);
+      "\"margin_errors\": %ld, \"hypot_checks\": %ld, \"hypot_errors\": %ld, "
+      "\"quadform_pass\": %ld, \"quadform_fail\": %ld, \"quadform_open\": %ld, "
+      "\"quadform_errors\": %ld}\n",
+      cells, at_one, hard, bisect, stopped, bad_plain, bad_queued, bad_replay,
+      audit[0], margin_bad, hyp_n, hyp_bad, quad_pass, quad_fail, quad_open, quad_bad);
   return 0;
 }

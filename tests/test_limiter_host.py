@@ -5,8 +5,8 @@ emits) and runs every limiter path of the kernels on per-cell limiter inputs
 dumped by the C oracle over a late-time jet march (rlmp_theta,
 solver.hpp:437-487).  Every path -- the plain 30-step bisection, the queued
 certified bisection (replay off) and the replayed bisection with its tail --
-must return the reference's theta bit for bit, the theta = 1 vertex
-certificate must never pass an infeasible cell, and the audit (the full
+must return the reference's theta bit for bit, the theta = 1 quadratic-form
+decision of the vertex floors must never contradict the exact checks, and the audit (the full
 feasible() re-run at every bisection step) must count zero disagreements.
 The GPU tests (test_gpu_march.py) check the same paths end to end on device.
 """
@@ -48,8 +48,10 @@ def test_limiter_paths_bit_exact(vo, limiter_check, tmp_path, m, steps, every):
     assert r["cells"] == len(recs) * g.nx * g.ny
     assert r["bisections"] > 1000  # late-time march: the bisection paths are exercised
     assert r["replay_stopped"] > 0  # ... including the tail resumption
-    assert r["certified_at_one"] > 0
+    # the quadratic form decides nearly every theta = 1 vertex check (both ways)
+    assert r["quadform_pass"] > 0.9 * r["theta_one"] and r["quadform_fail"] > 0
+    assert r["quadform_open"] < 0.02 * r["cells"]
     assert r["hypot_checks"] > 100000  # hypot_ref (conservative bound) == this host's libm
-    for k in ("certificate_errors", "mismatch_plain", "mismatch_queued", "mismatch_replay",
+    for k in ("quadform_errors", "mismatch_plain", "mismatch_queued", "mismatch_replay",
               "audit_errors", "margin_errors", "hypot_errors"):
         assert r[k] == 0, (k, r)
