@@ -31,7 +31,7 @@
 // W1 per-cell sort: 2 = 32-bit quantised keys + index through the bitonic
 // network, exact order restored among equal quantised keys (default);
 // 1 = per-lane sort + merge-path levels on 64-bit keys; 0 = 64-bit bitonic network
-#define VLBM_W1_SORT 1
+#define VLBM_W1_SORT 2
 #endif
 
 namespace vlbm_dev {
@@ -316,6 +316,102 @@ __device__ __forceinline__ void warp_merge_sort(unsigned long long (&v)[R], int 
   }
 }
 
+// Sorted column by QUANTISED keys: out[r] = the value of rank e = lane*R + r
+// among the M values col[0..M) (ranks >= M: unspecified).  The order-
+// preserving 64-bit key of each value is reduced to 22 bits relative to the
+// cell's own range (q = (key - base) >> sh; base = the smallest high word,
+// sh from the high-word span, both warp-uniform) and packed with the value's
+// slot as one 32-bit word c = q << 10 | slot, so the bitonic network's
+// compare-exchange is one integer min and one max (a 64-bit one costs 6-7
+// instructions).  q is monotone in the key, so the network leaves the values
+// in exact order except possibly inside runs of EQUAL q, which are contiguous:
+// the values are gathered by slot, and only if some adjacent pair of the warp
+// shares its q (rare: M <= 1024 values over 4 M buckets) the runs are put in
+// exact key order by odd-even transposition passes over the flagged pairs
+// until no pass swaps (after 6 passes: the 64-bit network on the gathered
+// values).  The result is the exact sorted order of the keys, as from the
+// 64-bit sorts.
+template <int R>
+__device__ __forceinline__ void warp_sort_quantised(int M, int lane, const double* col,
+                                                    double (&out)[R]) {
+  static_assert(R * 32 <= 1024, "slot index takes 10 bits");
+  static_assert(R >= 2, "the exact-order passes pair elements inside a lane");
+  unsigned c[R];
+  unsigned hmin = 0xffffffffu, hmax = 0u;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {  // the range of the keys' high words (the column is read twice)
+    const int m = r * 32 + lane;
+    if (m < M) {
+      const unsigned h = (unsigned)(dkey(col[m]) >> 32);
+      hmin = min(hmin, h);
+      hmax = max(hmax, h);
+    }
+  }
+  hmin = __reduce_min_sync(kFull, hmin);
+  hmax = __reduce_max_sync(kFull, hmax);
+  // key - base < (span + 1) 2^32 <= 2^(64 - clz(span))  ->  q < 2^22
+  const int sh = (64 - __clz(hmax - hmin)) - 22;  // 10 .. 42
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int m = r * 32 + lane;
+    const unsigned long long k = m < M ? dkey(col[m]) : 0ull;
+    const unsigned dh = (unsigned)(k >> 32) - hmin;
+    const unsigned q = sh >= 32 ? dh >> (sh - 32) : __funnelshift_r((unsigned)k, dh, sh);
+    c[r] = m < M ? (q << 10) | (unsigned)m : 0xffffffffu;  // pads last (slots < M <= 1023 there)
+  }
+  warp_sort_asc<R>(c, lane);
+  const int e0 = lane * R;
+#pragma unroll
+  for (int r = 0; r < R; ++r) out[r] = e0 + r < M ? col[c[r] & 1023u] : 0.0;
+  // adjacent ranks with equal q: bit r = pair (e0 + r, e0 + r + 1), both < M
+  const unsigned cnext = __shfl_down_sync(kFull, c[0], 1);
+  unsigned eq = 0u;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const unsigned cn = r + 1 < R ? c[r + 1] : cnext;
+    const bool in = e0 + r + 1 < M && (r + 1 < R || lane < 31);
+    eq |= (in && ((c[r] ^ cn) < 1024u)) ? 1u << r : 0u;
+  }
+  if (!__any_sync(kFull, eq != 0u)) return;
+  auto gt = [](double x, double y) { return dkey(x) > dkey(y); };
+  bool again = true;
+  for (int pass = 0; again; ++pass) {
+    if (pass == 6) {  // long runs (keys packed far below the cell's range): the 64-bit network
+      unsigned long long k[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) k[r] = e0 + r < M ? dkey(out[r]) : ~0ull;
+      warp_sort_asc<R>(k, lane);
+#pragma unroll
+      for (int r = 0; r < R; ++r) out[r] = dval(k[r]);
+      return;
+    }
+    bool sw = false;
+#pragma unroll
+    for (int par = 0; par < 2; ++par) {
+#pragma unroll
+      for (int r = par; r + 1 < R; r += 2) {
+        if ((eq >> r & 1u) && gt(out[r], out[r + 1])) {
+          const double t = out[r];
+          out[r] = out[r + 1];
+          out[r + 1] = t;
+          sw = true;
+        }
+      }
+      if (((R - 1) & 1) == par) {  // the pair across the lane boundary: (lane, R-1) with (lane+1, 0)
+        const double nx = __shfl_down_sync(kFull, out[0], 1);
+        const double pv = __shfl_up_sync(kFull, out[R - 1], 1);
+        const unsigned eqp = __shfl_up_sync(kFull, eq, 1);
+        const bool up = (eq >> (R - 1) & 1u) && gt(out[R - 1], nx);               // lower side
+        const bool dn = lane > 0 && (eqp >> (R - 1) & 1u) && gt(pv, out[0]);      // upper side
+        if (up) out[R - 1] = nx;
+        if (dn) out[0] = pv;
+        sw = sw || up || dn;
+      }
+    }
+    again = __any_sync(kFull, sw);
+  }
+}
+
 // Per-cell term: sum_m |a_(m) - b_(m)| over sorted ranks, sequential in m,
 // divided by M (metrics.hpp:118-122).  Loader functors return sample m's
 // value of the warp's cell.
@@ -327,6 +423,18 @@ __device__ __forceinline__ void warp_merge_sort(unsigned long long (&v)[R], int 
 // sequential in rank as in the reference.
 template <int R>
 __device__ __forceinline__ double w1_cell(int M, int lane, double* ca, const double* cb) {
+  double sb_[R];
+  if constexpr (VLBM_W1_SORT == 2 && R >= 2) {
+    {
+      double sa_[R];
+      warp_sort_quantised<R>(M, lane, ca, sa_);
+      __syncwarp();  // every lane has gathered from ca
+#pragma unroll
+      for (int r = 0; r < R; ++r) ca[r * 32 + lane] = sa_[r];
+      __syncwarp();
+    }
+    warp_sort_quantised<R>(M, lane, cb, sb_);
+  } else {
   unsigned long long k[R];
 #pragma unroll 1
   for (int pass = 0; pass < 2; ++pass) {
@@ -350,10 +458,13 @@ __device__ __forceinline__ double w1_cell(int M, int lane, double* ca, const dou
       __syncwarp();
     }
   }
+#pragma unroll
+  for (int r = 0; r < R; ++r) sb_[r] = dval(k[r]);
+  }
   // terms |a_(e) - b_(e)| in parallel, in place in ca (padded ranks
   // contribute nothing); then only the dependent adds run lane after lane
 #pragma unroll
-  for (int r = 0; r < R; ++r) ca[r * 32 + lane] = fabs(ca[r * 32 + lane] - dval(k[r]));
+  for (int r = 0; r < R; ++r) ca[r * 32 + lane] = fabs(ca[r * 32 + lane] - sb_[r]);
   __syncwarp();
   const int valid = M - lane * R;  // ranks of this lane that exist
   double cell = 0.0;

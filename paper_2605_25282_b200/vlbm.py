@@ -412,9 +412,8 @@ class BatchSimulation:
         _check(lib().vlbm_batch_audit(self._h, n))
         return dict(mismatches=n[0], bisections=n[1], certified_at_thc=n[2], uncertified=n[3],
                     not_certifiable=n[4], no_margin_at_0=n[5], unc_vertices_start=n[6],
-                    vertex_evals=n[7], diag_ok_at_1=n[8], vertex_certified_at_1=n[9],
-                    feasible_at_1=n[10], warps_with_vertex_checks=n[11],
-                    unc_feasible=n[12], unc_feasible_loose=n[13], unc_feasible_quad=n[14])
+                    vertex_evals=n[7], diag_ok_at_1=n[8], vertex_decided_at_1=n[9],
+                    feasible_at_1=n[10], vertex_open_at_1=n[12])
 
     def audit_mismatches(self) -> int:
         return self.audit_counters()["mismatches"]

@@ -81,6 +81,31 @@ def test_wasserstein1_bitwise(vlbm, oc, M, ties):
         assert bits(got) == bits(want), (M, var, got, want)
 
 
+@pytest.mark.parametrize("M", [40, 100, 1000, 1024])
+def test_wasserstein1_bitwise_packed_values(vlbm, oc, M):
+    """Values packed far below the cell's range (adjacent doubles next to a
+    few outliers, mixed signs around zero): the W1 sort's quantised keys
+    collide in long runs, so its exact-order passes and the 64-bit fallback
+    decide the order (post.cu::warp_sort_quantised)."""
+    rng = np.random.default_rng(100 + M)
+    ny, nx = 4, 6
+
+    def packed():
+        x = np.ones((M, 4, ny, nx))
+        k = rng.integers(0, 48, size=(M, ny, nx))
+        x[:, 0] = 1.0 + k * 2.0 ** -52                     # <= 48 distinct adjacent doubles
+        x[:3, 0] = np.array([1e6, -3.0, 7.5])[:, None, None]  # outliers stretch the range
+        x[:, 0, 1] = 1.0 + rng.permutation(M)[:, None] * 2.0 ** -52   # M distinct, one run
+        x[:, 0, 2] = (rng.integers(-20, 20, size=(M, nx))) * 5e-324   # +-denormals and zeros
+        x[:, 0, 3, :3] = rng.lognormal(-0.125, 0.5, size=(M, 3))      # ordinary cells beside them
+        return x
+
+    a, b = packed(), packed()
+    got = vlbm.wasserstein1(a, b, 0)
+    want = oc.wasserstein1(a, b, 0)
+    assert bits(got) == bits(want), (M, got, want)
+
+
 def test_wasserstein1_kats_and_ot(vlbm, ref):
     """test_metrics.cpp:106-122: hand values and the brute-force OT oracle."""
     def w1s(x, y):
