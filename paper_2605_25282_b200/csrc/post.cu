@@ -316,6 +316,71 @@ __device__ __forceinline__ void warp_merge_sort(unsigned long long (&v)[R], int 
   }
 }
 
+// The same ascending bitonic network on 32-bit keys, laid out for a small
+// code footprint: the fully unrolled network is ~2.8 k instructions per sort
+// and the kernel then stalls on instruction fetch (ncu: no_instruction 3.9
+// cycles per issue), so the cross-lane steps run as runtime loops over the
+// partner distance (one shuffle + one min/max per key, 2 R instructions per
+// body) and the in-register half-cleaners that end every merge size share one
+// body.  Only the in-register stages need compile-time register indices.
+template <int R>
+__device__ __forceinline__ void warp_sort_u32(unsigned (&v)[R], int lane) {
+  auto cas = [](unsigned& lo, unsigned& hi) {
+    const unsigned a = lo, b = hi;
+    lo = min(a, b);
+    hi = max(a, b);
+  };
+  // runs of R keys sorted inside each lane (merge sizes 2 .. R)
+#pragma unroll
+  for (int k = 2; k <= R; k <<= 1) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int r2 = r ^ (k - 1);
+      if (r < r2) cas(v[r], v[r2]);
+    }
+#pragma unroll
+    for (int j = k >> 2; j > 0; j >>= 1) {
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if ((r & j) == 0) cas(v[r], v[r | j]);
+    }
+  }
+  // merge sizes 2R .. 32R: flip across lanes (partner lane ^ (2g - 1), mirrored
+  // register), half-cleaners across lanes (partner lane ^ h), then in registers
+#pragma unroll 1
+  for (int g = 1; g < 32; g <<= 1) {  // g = k / (2R): lanes per half of the merged block
+    {
+      const int m = 2 * g - 1;
+      const bool upper = (lane & g) != 0;
+#pragma unroll
+      for (int r = 0; r < (R + 1) / 2; ++r) {
+        const int q = R - 1 - r;
+        const unsigned o1 = __shfl_xor_sync(kFull, v[q], m);
+        if (q != r) {
+          const unsigned o2 = __shfl_xor_sync(kFull, v[r], m);
+          v[q] = upper ? max(v[q], o2) : min(v[q], o2);
+        }
+        v[r] = upper ? max(v[r], o1) : min(v[r], o1);
+      }
+    }
+#pragma unroll 1
+    for (int h = g >> 1; h > 0; h >>= 1) {
+      const bool upper = (lane & h) != 0;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const unsigned o = __shfl_xor_sync(kFull, v[r], h);
+        v[r] = upper ? max(v[r], o) : min(v[r], o);
+      }
+    }
+#pragma unroll
+    for (int j = R >> 1; j > 0; j >>= 1) {
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if ((r & j) == 0) cas(v[r], v[r | j]);
+    }
+  }
+}
+
 // Sorted column by QUANTISED keys: out[r] = the value of rank e = lane*R + r
 // among the M values col[0..M) (ranks >= M: unspecified).  The order-
 // preserving 64-bit key of each value is reduced to 22 bits relative to the
@@ -328,11 +393,11 @@ __device__ __forceinline__ void warp_merge_sort(unsigned long long (&v)[R], int 
 // the values are gathered by slot, and only if some adjacent pair of the warp
 // shares its q (rare: M <= 1024 values over 4 M buckets) the runs are put in
 // exact key order by odd-even transposition passes over the flagged pairs
-// until no pass swaps (after 6 passes: the 64-bit network on the gathered
-// values).  The result is the exact sorted order of the keys, as from the
-// 64-bit sorts.
+// until no pass swaps (after 6 passes: the 64-bit merge sort of the gathered
+// values, with col as its scratch).  The result is the exact sorted order of
+// the keys, as from the 64-bit sorts; col is clobbered.
 template <int R>
-__device__ __forceinline__ void warp_sort_quantised(int M, int lane, const double* col,
+__device__ __forceinline__ void warp_sort_quantised(int M, int lane, double* col,
                                                     double (&out)[R]) {
   static_assert(R * 32 <= 1024, "slot index takes 10 bits");
   static_assert(R >= 2, "the exact-order passes pair elements inside a lane");
@@ -359,7 +424,7 @@ __device__ __forceinline__ void warp_sort_quantised(int M, int lane, const doubl
     const unsigned q = sh >= 32 ? dh >> (sh - 32) : __funnelshift_r((unsigned)k, dh, sh);
     c[r] = m < M ? (q << 10) | (unsigned)m : 0xffffffffu;  // pads last (slots < M <= 1023 there)
   }
-  warp_sort_asc<R>(c, lane);
+  warp_sort_u32<R>(c, lane);
   const int e0 = lane * R;
 #pragma unroll
   for (int r = 0; r < R; ++r) out[r] = e0 + r < M ? col[c[r] & 1023u] : 0.0;
@@ -376,11 +441,13 @@ __device__ __forceinline__ void warp_sort_quantised(int M, int lane, const doubl
   auto gt = [](double x, double y) { return dkey(x) > dkey(y); };
   bool again = true;
   for (int pass = 0; again; ++pass) {
-    if (pass == 6) {  // long runs (keys packed far below the cell's range): the 64-bit network
+    if (pass == 6) {  // long runs (values packed far below the cell's range): the 64-bit
+                      // merge sort of the gathered values; col is free (every lane gathered)
       unsigned long long k[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) k[r] = e0 + r < M ? dkey(out[r]) : ~0ull;
-      warp_sort_asc<R>(k, lane);
+      __syncwarp();
+      warp_merge_sort<R>(k, lane, reinterpret_cast<unsigned long long*>(col));
 #pragma unroll
       for (int r = 0; r < R; ++r) out[r] = dval(k[r]);
       return;
@@ -422,18 +489,19 @@ __device__ __forceinline__ void warp_sort_quantised(int M, int lane, const doubl
 // visits lanes in order, each adding its R terms, so the sum is strictly
 // sequential in rank as in the reference.
 template <int R>
-__device__ __forceinline__ double w1_cell(int M, int lane, double* ca, const double* cb) {
+__device__ __forceinline__ double w1_cell(int M, int lane, double* ca, double* cb) {
   double sb_[R];
   if constexpr (VLBM_W1_SORT == 2 && R >= 2) {
-    {
-      double sa_[R];
-      warp_sort_quantised<R>(M, lane, ca, sa_);
-      __syncwarp();  // every lane has gathered from ca
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {  // one copy of the network's code for both columns
+      warp_sort_quantised<R>(M, lane, pass ? cb : ca, sb_);
+      if (pass == 0) {
+        __syncwarp();  // every lane has gathered from ca
 #pragma unroll
-      for (int r = 0; r < R; ++r) ca[r * 32 + lane] = sa_[r];
-      __syncwarp();
+        for (int r = 0; r < R; ++r) ca[r * 32 + lane] = sb_[r];
+        __syncwarp();
+      }
     }
-    warp_sort_quantised<R>(M, lane, cb, sb_);
   } else {
   unsigned long long k[R];
 #pragma unroll 1
@@ -461,19 +529,24 @@ __device__ __forceinline__ double w1_cell(int M, int lane, double* ca, const dou
 #pragma unroll
   for (int r = 0; r < R; ++r) sb_[r] = dval(k[r]);
   }
-  // terms |a_(e) - b_(e)| in parallel, in place in ca (padded ranks
-  // contribute nothing); then only the dependent adds run lane after lane
-#pragma unroll
-  for (int r = 0; r < R; ++r) ca[r * 32 + lane] = fabs(ca[r * 32 + lane] - sb_[r]);
-  __syncwarp();
+  // terms |a_(e) - b_(e)| of the lane's own ranks in registers, all lanes in
+  // parallel (padded ranks contribute nothing); then only the dependent adds
+  // run lane after lane
   const int valid = M - lane * R;  // ranks of this lane that exist
+#pragma unroll
+  for (int r = 0; r < R; ++r) sb_[r] = fabs(ca[r * 32 + lane] - sb_[r]);
   double cell = 0.0;
 #pragma unroll 1
   for (int L = 0; L < 32; ++L) {
     if (lane == L) {
+      if (valid >= R) {  // a full lane: R unguarded dependent adds
 #pragma unroll
-      for (int r = 0; r < R; ++r)
-        if (r < valid) cell += ca[r * 32 + L];
+        for (int r = 0; r < R; ++r) cell += sb_[r];
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if (r < valid) cell += sb_[r];
+      }
     }
     cell = __shfl_sync(kFull, cell, L);
   }
@@ -495,27 +568,21 @@ __device__ __forceinline__ double w1_cell(int M, int lane, double* ca, const dou
 //            restriction is fused as in kind 1
 constexpr int kW1Cells = 4;
 
-// Sample m's value pair of (launch-local) cell c for the W1 kernels.
+// Sample m's value pair of (launch-local) cell c for the W1 kernels; (i, j):
+// the cell's coarse coordinates (kinds 1 and 3), found once per thread.
 template <int kKind>
-__device__ __forceinline__ void w1_load(int M, long long c, int m, int nxc, const double* a,
-                                        long long as, const double* b, long long bs,
-                                        double& va, double& vb) {
+__device__ __forceinline__ void w1_load(int M, long long c, int m, int nxc, int i, int j,
+                                        const double* a, long long as, const double* b,
+                                        long long bs, double& va, double& vb) {
   if (kKind == 2) {
     va = a[c * M + m];
     vb = b[c * M + m];
   } else if (kKind == 3) {
-    const long long cg = as + c;
-    const int j = (int)(cg / nxc), i = (int)(cg - (long long)j * nxc);
-    va = reinterpret_cast<const double* const*>(a)[m][cg];
+    va = reinterpret_cast<const double* const*>(a)[m][as + c];
     vb = restrict_at(reinterpret_cast<const double* const*>(b)[m], 2 * nxc, i, j);
   } else {
     va = a[(long long)m * as + c];
-    if (kKind == 1) {
-      const int j = (int)(c / nxc), i = (int)(c - (long long)j * nxc);
-      vb = restrict_at(b + (long long)m * bs, 2 * nxc, i, j);
-    } else {
-      vb = b[(long long)m * bs + c];
-    }
+    vb = kKind == 1 ? restrict_at(b + (long long)m * bs, 2 * nxc, i, j) : b[(long long)m * bs + c];
   }
 }
 
@@ -529,21 +596,47 @@ __global__ void __launch_bounds__(32 * kW1Cells, 4) k_w1_tile(int M, long long n
   double* sa = smw;
   double* sb = smw + kW1Cells * LD;
   const long long c0 = (long long)blockIdx.x * kW1Cells;
+  if (kKind == 2) {
 #pragma unroll 4
-  for (int e = threadIdx.x; e < M * kW1Cells; e += blockDim.x) {
-    int m, cl;
-    if (kKind == 2) {
-      cl = e / M;
-      m = e - cl * M;
-    } else {
-      m = e / kW1Cells;
-      cl = e - m * kW1Cells;
+    for (int e = threadIdx.x; e < M * kW1Cells; e += blockDim.x) {
+      const int cl = e / M, m = e - cl * M;
+      const long long c = c0 + cl;
+      double va = 0.0, vb = 0.0;
+      if (c < n) w1_load<kKind>(M, c, m, nxc, 0, 0, a, as, b, bs, va, vb);
+      sa[cl * LD + m] = va;
+      sb[cl * LD + m] = vb;
     }
+  } else {
+    // element e = m * kW1Cells + cl with e = threadIdx.x + k * blockDim.x: a
+    // thread keeps ONE cell (cl) for all its samples, so the cell's coarse
+    // coordinates (a 64-bit division) are found once; kStage samples' loads
+    // are issued before the first is stored (the staging is latency-bound)
+    constexpr int kStage = 8, kStep = 32;  // kStep = blockDim.x / kW1Cells samples apart
+    const int cl = threadIdx.x % kW1Cells;
     const long long c = c0 + cl;
-    double va = 0.0, vb = 0.0;
-    if (c < n) w1_load<kKind>(M, c, m, nxc, a, as, b, bs, va, vb);
-    sa[cl * LD + m] = va;
-    sb[cl * LD + m] = vb;
+    int i = 0, j = 0;
+    if (kKind != 0 && c < n) {
+      const long long cg = (kKind == 3 ? as : 0) + c;
+      j = (int)(cg / nxc);
+      i = (int)(cg - (long long)j * nxc);
+    }
+    for (int m0 = threadIdx.x / kW1Cells; m0 < M; m0 += kStage * kStep) {
+      double va[kStage], vb[kStage];
+#pragma unroll
+      for (int q = 0; q < kStage; ++q) {
+        const int m = m0 + q * kStep;
+        va[q] = vb[q] = 0.0;
+        if (m < M && c < n) w1_load<kKind>(M, c, m, nxc, i, j, a, as, b, bs, va[q], vb[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < kStage; ++q) {
+        const int m = m0 + q * kStep;
+        if (m < M) {
+          sa[cl * LD + m] = va[q];
+          sb[cl * LD + m] = vb[q];
+        }
+      }
+    }
   }
   __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -692,13 +785,19 @@ __global__ void k_w1_keys(int M, long long c0, long long nb, int nxc, const doub
   const long long cb = (long long)blockIdx.x * 32;  // batch-local cell tile
   const int mb = blockIdx.y * 32;                    // sample tile
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads
+  int ci = 0, cj = 0;  // coarse coordinates of this thread's cell (kinds 1 and 3)
+  if ((kKind == 1 || kKind == 3) && cb + tx < nb) {
+    const long long cg = (kKind == 3 ? as : 0) + c0 + cb + tx;
+    cj = (int)(cg / nxc);
+    ci = (int)(cg - (long long)cj * nxc);
+  }
   for (int r = ty; r < 32; r += 8) {  // read: sample mb + r, cell cb + tx
     const int m = mb + r;
     const long long cl = cb + tx, c = c0 + cl;
     unsigned long long va = 0, vb = 0;
     if (m < M && cl < nb) {
       double x, y;
-      w1_load<kKind>(M, c, m, nxc, a, as, b, bs, x, y);
+      w1_load<kKind>(M, c, m, nxc, ci, cj, a, as, b, bs, x, y);
       va = dkey(x);
       vb = dkey(y);
     }
