@@ -335,7 +335,34 @@ __global__ void __launch_bounds__(tiled::NTT, VLBM_THETA_MINB)
       return add(add(a, b), scale(al, plane4(R, NR2, rq(x, y))));
     };
     const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
-    cs foC = ufo_at(tx, ty);
+    // This cell's four incoming Maxwellians, formed ONCE: they give both its
+    // u_FO (compute_candidates) and its face corrections (face_corrections
+    // :321-329), so the corrections are taken here, before the barrier.
+    const int i = x0 + tx, j = y0 + ty;
+    const bool valid = i < P.nx && j < P.ny;
+    cs cf[4];
+    cs foC;
+    {
+      auto pop = [&](int k, int x, int y) {
+        if (VLBM_THETA_GPOP) {
+          const int ii = x0 + x, jj = y0 + y;
+          if (ii >= 0 && ii < P.nx && jj >= 0 && jj < P.ny)
+            return load_plane4(src + (4 + 4 * k) * P.plane, P.plane, (long long)jj * P.pitch + ii);
+          return load_pop(P, src, rows, k, ii, jj, inv2a);
+        }
+        return plane4(SP + 4 * k * NAT, NAT, (y + 1) * AX + (x + 2));
+      };
+      const int qc = rq(tx, ty);
+      const cs mw = M(rq(tx - 1, ty), 0), me = M(rq(tx + 1, ty), 1);
+      const cs ms = M(rq(tx, ty - 1), 2), mn = M(rq(tx, ty + 1), 3);
+      foC = add(add(add(mw, me), add(ms, mn)), scale(al, plane4(R, NR2, qc)));
+      if (valid) {
+        cf[0] = sub(sub(mw, pop(0, tx - 1, ty)), sub(M(qc, 1), pop(1, tx, ty)));
+        cf[1] = sub(sub(me, pop(1, tx + 1, ty)), sub(M(qc, 0), pop(0, tx, ty)));
+        cf[2] = sub(sub(ms, pop(2, tx, ty - 1)), sub(M(qc, 3), pop(3, tx, ty)));
+        cf[3] = sub(sub(mn, pop(3, tx, ty + 1)), sub(M(qc, 2), pop(2, tx, ty)));
+      }
+    }
     RF[fq(tx, ty)] = foC.r;
     RF[NF + fq(tx, ty)] = pressure(foC, gm1);
     if (threadIdx.x < 2 * TX + 2 * TYT) {
@@ -356,28 +383,12 @@ __global__ void __launch_bounds__(tiled::NTT, VLBM_THETA_MINB)
     }
     __syncthreads();
 
-    // Limiter inputs of this thread's cell (face_corrections :321-329,
-    // rlmp_bounds :364-435): the last reads of the staged tile.
-    const int i = x0 + tx, j = y0 + ty;
-    const bool valid = i < P.nx && j < P.ny;
-    cs cf[4], delta;
+    // Limiter inputs of this thread's cell (rlmp_bounds :364-435): the last
+    // reads of the staged tile.
+    cs delta;
     RlmpBounds b;
     bool hard = false;
     if (valid) {
-      auto pop = [&](int k, int x, int y) {
-        if (VLBM_THETA_GPOP) {
-          const int ii = x0 + x, jj = y0 + y;
-          if (ii >= 0 && ii < P.nx && jj >= 0 && jj < P.ny)
-            return load_plane4(src + (4 + 4 * k) * P.plane, P.plane, (long long)jj * P.pitch + ii);
-          return load_pop(P, src, rows, k, ii, jj, inv2a);
-        }
-        return plane4(SP + 4 * k * NAT, NAT, (y + 1) * AX + (x + 2));
-      };
-      const int qc = rq(tx, ty);
-      cf[0] = sub(sub(M(rq(tx - 1, ty), 0), pop(0, tx - 1, ty)), sub(M(qc, 1), pop(1, tx, ty)));
-      cf[1] = sub(sub(M(rq(tx + 1, ty), 1), pop(1, tx + 1, ty)), sub(M(qc, 0), pop(0, tx, ty)));
-      cf[2] = sub(sub(M(rq(tx, ty - 1), 2), pop(2, tx, ty - 1)), sub(M(qc, 3), pop(3, tx, ty)));
-      cf[3] = sub(sub(M(rq(tx, ty + 1), 3), pop(3, tx, ty + 1)), sub(M(qc, 2), pop(2, tx, ty)));
       RlmpStencil st;
       st.fo = foC;
       const int fpts[5] = {fq(tx, ty), fq(tx - 1, ty), fq(tx + 1, ty), fq(tx, ty - 1),

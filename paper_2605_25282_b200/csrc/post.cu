@@ -27,12 +27,6 @@
 
 #include "internal.h"
 
-#ifndef VLBM_W1_SORT
-// W1 per-cell sort: 2 = 32-bit quantised keys + index through the bitonic
-// network, exact order restored among equal quantised keys (default);
-// 1 = per-lane sort + merge-path levels on 64-bit keys; 0 = 64-bit bitonic network
-#define VLBM_W1_SORT 2
-#endif
 
 namespace vlbm_dev {
 
@@ -381,54 +375,54 @@ __device__ __forceinline__ void warp_sort_u32(unsigned (&v)[R], int lane) {
   }
 }
 
-// Sorted column by QUANTISED keys: out[r] = the value of rank e = lane*R + r
-// among the M values col[0..M) (ranks >= M: unspecified).  The order-
-// preserving 64-bit key of each value is reduced to 22 bits relative to the
-// cell's own range (q = (key - base) >> sh; base = the smallest high word,
-// sh from the high-word span, both warp-uniform) and packed with the value's
-// slot as one 32-bit word c = q << 10 | slot, so the bitonic network's
-// compare-exchange is one integer min and one max (a 64-bit one costs 6-7
-// instructions).  q is monotone in the key, so the network leaves the values
-// in exact order except possibly inside runs of EQUAL q, which are contiguous:
-// the values are gathered by slot, and only if some adjacent pair of the warp
-// shares its q (rare: M <= 1024 values over 4 M buckets) the runs are put in
-// exact key order by odd-even transposition passes over the flagged pairs
-// until no pass swaps (after 6 passes: the 64-bit merge sort of the gathered
-// values, with col as its scratch).  The result is the exact sorted order of
-// the keys, as from the 64-bit sorts; col is clobbered.
+// Exact rank order of a cell's column by QUANTISED keys.  On return (true)
+// c[r] & 1023 is the slot of the value of rank e = lane*R + r among the M
+// values col[0..M) (ranks >= M: c[r] = ~0).  The order-preserving 64-bit key
+// of each value is reduced to 22 bits relative to the cell's own key range
+// (q = (key - kmin) >> sh with sh from the span kmax - kmin, warp-uniform) and
+// packed with the value's slot as one 32-bit word c = q << 10 | slot, so the
+// bitonic network's compare-exchange is one integer min and one max (a 64-bit
+// one costs 6-7 instructions).  q is monotone in the key, so the network
+// leaves the slots in exact key order except possibly inside runs of EQUAL q,
+// which are contiguous: only if some adjacent pair of the warp shares its q
+// (rare: M <= 1024 values over 4 M buckets; never when the whole span is below
+// 2^22 ulps, where q is the exact offset) the runs are put in exact order by
+// odd-even transposition passes over the flagged pairs, comparing the values'
+// keys through the column, until no pass swaps.  After 6 passes (long runs:
+// values packed far below the cell's range) it gives up and returns false: the
+// caller sorts the column with the 64-bit merge sort instead.
 template <int R>
-__device__ __forceinline__ void warp_sort_quantised(int M, int lane, double* col,
-                                                    double (&out)[R]) {
+__device__ __forceinline__ bool warp_sort_slots(int M, int lane, const double* col,
+                                                unsigned (&c)[R]) {
   static_assert(R * 32 <= 1024, "slot index takes 10 bits");
   static_assert(R >= 2, "the exact-order passes pair elements inside a lane");
-  unsigned c[R];
-  unsigned hmin = 0xffffffffu, hmax = 0u;
+  unsigned long long kmin = ~0ull, kmax = 0ull;
 #pragma unroll
-  for (int r = 0; r < R; ++r) {  // the range of the keys' high words (the column is read twice)
+  for (int r = 0; r < R; ++r) {  // the key range (the column is read twice)
     const int m = r * 32 + lane;
     if (m < M) {
-      const unsigned h = (unsigned)(dkey(col[m]) >> 32);
-      hmin = min(hmin, h);
-      hmax = max(hmax, h);
+      const unsigned long long k = dkey(col[m]);
+      kmin = min(kmin, k);
+      kmax = max(kmax, k);
     }
   }
-  hmin = __reduce_min_sync(kFull, hmin);
-  hmax = __reduce_max_sync(kFull, hmax);
-  // key - base < (span + 1) 2^32 <= 2^(64 - clz(span))  ->  q < 2^22
-  const int sh = (64 - __clz(hmax - hmin)) - 22;  // 10 .. 42
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    kmin = min(kmin, __shfl_xor_sync(kFull, kmin, o));
+    kmax = max(kmax, __shfl_xor_sync(kFull, kmax, o));
+  }
+  // key - kmin <= span < 2^(64 - clz(span))  ->  q < 2^22
+  const int sh = max(0, 42 - __clzll((long long)(kmax - kmin)));
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int m = r * 32 + lane;
-    const unsigned long long k = m < M ? dkey(col[m]) : 0ull;
-    const unsigned dh = (unsigned)(k >> 32) - hmin;
-    const unsigned q = sh >= 32 ? dh >> (sh - 32) : __funnelshift_r((unsigned)k, dh, sh);
-    c[r] = m < M ? (q << 10) | (unsigned)m : 0xffffffffu;  // pads last (slots < M <= 1023 there)
+    const unsigned long long d = (m < M ? dkey(col[m]) : kmin) - kmin;
+    c[r] = m < M ? ((unsigned)(d >> sh) << 10) | (unsigned)m
+                 : 0xffffffffu;  // pads last (slots < M <= 1023 when there are pads)
   }
   warp_sort_u32<R>(c, lane);
-  const int e0 = lane * R;
-#pragma unroll
-  for (int r = 0; r < R; ++r) out[r] = e0 + r < M ? col[c[r] & 1023u] : 0.0;
   // adjacent ranks with equal q: bit r = pair (e0 + r, e0 + r + 1), both < M
+  const int e0 = lane * R;
   const unsigned cnext = __shfl_down_sync(kFull, c[0], 1);
   unsigned eq = 0u;
 #pragma unroll
@@ -437,115 +431,96 @@ __device__ __forceinline__ void warp_sort_quantised(int M, int lane, double* col
     const bool in = e0 + r + 1 < M && (r + 1 < R || lane < 31);
     eq |= (in && ((c[r] ^ cn) < 1024u)) ? 1u << r : 0u;
   }
-  if (!__any_sync(kFull, eq != 0u)) return;
-  auto gt = [](double x, double y) { return dkey(x) > dkey(y); };
+  if (!__any_sync(kFull, eq != 0u)) return true;
+  auto gt = [&](unsigned x, unsigned y) { return dkey(col[x & 1023u]) > dkey(col[y & 1023u]); };
   bool again = true;
+#pragma unroll 1
   for (int pass = 0; again; ++pass) {
-    if (pass == 6) {  // long runs (values packed far below the cell's range): the 64-bit
-                      // merge sort of the gathered values; col is free (every lane gathered)
-      unsigned long long k[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r) k[r] = e0 + r < M ? dkey(out[r]) : ~0ull;
-      __syncwarp();
-      warp_merge_sort<R>(k, lane, reinterpret_cast<unsigned long long*>(col));
-#pragma unroll
-      for (int r = 0; r < R; ++r) out[r] = dval(k[r]);
-      return;
-    }
+    if (pass == 6) return false;
     bool sw = false;
 #pragma unroll
     for (int par = 0; par < 2; ++par) {
 #pragma unroll
       for (int r = par; r + 1 < R; r += 2) {
-        if ((eq >> r & 1u) && gt(out[r], out[r + 1])) {
-          const double t = out[r];
-          out[r] = out[r + 1];
-          out[r + 1] = t;
+        if ((eq >> r & 1u) && gt(c[r], c[r + 1])) {
+          const unsigned t = c[r];
+          c[r] = c[r + 1];
+          c[r + 1] = t;
           sw = true;
         }
       }
       if (((R - 1) & 1) == par) {  // the pair across the lane boundary: (lane, R-1) with (lane+1, 0)
-        const double nx = __shfl_down_sync(kFull, out[0], 1);
-        const double pv = __shfl_up_sync(kFull, out[R - 1], 1);
+        const unsigned nx = __shfl_down_sync(kFull, c[0], 1);
+        const unsigned pv = __shfl_up_sync(kFull, c[R - 1], 1);
         const unsigned eqp = __shfl_up_sync(kFull, eq, 1);
-        const bool up = (eq >> (R - 1) & 1u) && gt(out[R - 1], nx);               // lower side
-        const bool dn = lane > 0 && (eqp >> (R - 1) & 1u) && gt(pv, out[0]);      // upper side
-        if (up) out[R - 1] = nx;
-        if (dn) out[0] = pv;
+        const bool up = (eq >> (R - 1) & 1u) && gt(c[R - 1], nx);           // lower side
+        const bool dn = lane > 0 && (eqp >> (R - 1) & 1u) && gt(pv, c[0]);  // upper side
+        if (up) c[R - 1] = nx;
+        if (dn) c[0] = pv;
         sw = sw || up || dn;
       }
     }
     again = __any_sync(kFull, sw);
   }
+  return true;
+}
+
+// out[r] = the value of rank lane*R + r of the column (ranks >= M: +0), exact
+// key order: warp_sort_slots + a gather by slot; the 64-bit sorts for long
+// runs of equal quantised keys (merge sort, col is its scratch and is
+// clobbered) and for R = 1 (the network).  All lanes of the warp call it.
+template <int R>
+__device__ __forceinline__ void warp_sort_column(int M, int lane, double* col, double (&out)[R]) {
+  bool done = false;
+  if constexpr (R >= 2) {
+    unsigned c[R];
+    done = warp_sort_slots<R>(M, lane, col, c);
+    if (done) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) out[r] = lane * R + r < M ? col[c[r] & 1023u] : 0.0;
+    }
+  }
+  if (!done) {
+    unsigned long long k[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int m = r * 32 + lane;
+      k[r] = m < M ? dkey(col[m]) : ~0ull;
+    }
+    if constexpr (R >= 2) {
+      __syncwarp();  // the column is free once every lane holds its keys
+      warp_merge_sort<R>(k, lane, reinterpret_cast<unsigned long long*>(col));
+    } else {
+      warp_sort_asc<R>(k, lane);
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) out[r] = lane * R + r < M ? dval(k[r]) : 0.0;
+  }
 }
 
 // Per-cell term: sum_m |a_(m) - b_(m)| over sorted ranks, sequential in m,
-// divided by M (metrics.hpp:118-122).  Loader functors return sample m's
-// value of the warp's cell.
-// ca / cb: the cell's M values of each ensemble in shared memory (ca is
-// overwritten).  One ensemble is sorted at a time (R keys per lane in
-// registers); the sorted first column is parked in ca at slot (r, lane) so the
-// second sort has the registers to itself.  Rank e = lane*R + r; the chain
-// visits lanes in order, each adding its R terms, so the sum is strictly
+// divided by M (metrics.hpp:118-122), from the lane's sorted values of both
+// ensembles (rank e = lane*R + r): the terms in parallel, then the chain
+// visits the lanes in order, each adding its R terms, so the sum is strictly
 // sequential in rank as in the reference.
 template <int R>
-__device__ __forceinline__ double w1_cell(int M, int lane, double* ca, double* cb) {
-  double sb_[R];
-  if constexpr (VLBM_W1_SORT == 2 && R >= 2) {
-#pragma unroll 1
-    for (int pass = 0; pass < 2; ++pass) {  // one copy of the network's code for both columns
-      warp_sort_quantised<R>(M, lane, pass ? cb : ca, sb_);
-      if (pass == 0) {
-        __syncwarp();  // every lane has gathered from ca
-#pragma unroll
-        for (int r = 0; r < R; ++r) ca[r * 32 + lane] = sb_[r];
-        __syncwarp();
-      }
-    }
-  } else {
-  unsigned long long k[R];
-#pragma unroll 1
-  for (int pass = 0; pass < 2; ++pass) {
-    const double* col = pass ? cb : ca;
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int m = r * 32 + lane;  // load slot order is free: sorting is order-free
-      k[r] = m < M ? dkey(col[m]) : ~0ull;
-    }
-#if VLBM_W1_SORT == 1
-    __syncwarp();  // the column is free once every lane holds its keys
-    warp_merge_sort<R>(k, lane,
-                       reinterpret_cast<unsigned long long*>(const_cast<double*>(col)));
-#else
-    warp_sort_asc<R>(k, lane);
-#endif
-    if (pass == 0) {
-      __syncwarp();
-#pragma unroll
-      for (int r = 0; r < R; ++r) ca[r * 32 + lane] = dval(k[r]);
-      __syncwarp();
-    }
-  }
-#pragma unroll
-  for (int r = 0; r < R; ++r) sb_[r] = dval(k[r]);
-  }
-  // terms |a_(e) - b_(e)| of the lane's own ranks in registers, all lanes in
-  // parallel (padded ranks contribute nothing); then only the dependent adds
-  // run lane after lane
+__device__ __forceinline__ double w1_rank_sum(int M, int lane, const double (&sa)[R],
+                                              const double (&sb)[R]) {
   const int valid = M - lane * R;  // ranks of this lane that exist
+  double t[R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) sb_[r] = fabs(ca[r * 32 + lane] - sb_[r]);
+  for (int r = 0; r < R; ++r) t[r] = fabs(sa[r] - sb[r]);
   double cell = 0.0;
 #pragma unroll 1
   for (int L = 0; L < 32; ++L) {
     if (lane == L) {
       if (valid >= R) {  // a full lane: R unguarded dependent adds
 #pragma unroll
-        for (int r = 0; r < R; ++r) cell += sb_[r];
+        for (int r = 0; r < R; ++r) cell += t[r];
       } else {
 #pragma unroll
         for (int r = 0; r < R; ++r)
-          if (r < valid) cell += sb_[r];
+          if (r < valid) cell += t[r];
       }
     }
     cell = __shfl_sync(kFull, cell, L);
@@ -553,9 +528,13 @@ __device__ __forceinline__ double w1_cell(int M, int lane, double* ca, double* c
   return cell / static_cast<double>(M);
 }
 
-// A CTA of kW1Cells warps owns kW1Cells consecutive cells, one warp per cell.
-// The M values of both ensembles for its cells are staged into shared memory
-// [cell][m] with sector-efficient loads, then each warp reduces its cell.
+// A CTA of kW1Cells warps owns kW1Cells consecutive cells, one warp per cell,
+// with ONE shared-memory column [m] per cell (8.4 KB at M <= 1024: 16 warps
+// per SM where two columns allowed 12).  The M values of the first ensemble
+// for the CTA's cells are staged into the columns with sector-efficient loads
+// and each warp sorts its cell's column into registers; then the second
+// ensemble is staged into the SAME columns, sorted, and each warp adds its
+// cell's |a_(m) - b_(m)| in rank order.
 //   kKind 0: sample-major planes, value(m, c) = a[m*as + c], b[m*bs + c]
 //   kKind 1: coarse planes vs the restriction of fine planes (b = fine,
 //            bs = fine sample stride; 32-byte coarse and two 64-byte fine
@@ -568,21 +547,60 @@ __device__ __forceinline__ double w1_cell(int M, int lane, double* ca, double* c
 //            restriction is fused as in kind 1
 constexpr int kW1Cells = 4;
 
-// Sample m's value pair of (launch-local) cell c for the W1 kernels; (i, j):
-// the cell's coarse coordinates (kinds 1 and 3), found once per thread.
-template <int kKind>
-__device__ __forceinline__ void w1_load(int M, long long c, int m, int nxc, int i, int j,
-                                        const double* a, long long as, const double* b,
-                                        long long bs, double& va, double& vb) {
+// Sample m's value of (launch-local) cell c in ensemble kB ? b : a; (i, j): the
+// cell's coarse coordinates (kinds 1 and 3), found once per thread.
+template <int kKind, bool kB>
+__device__ __forceinline__ double w1_load(int M, long long c, int m, int nxc, int i, int j,
+                                          const double* a, long long as, const double* b,
+                                          long long bs) {
+  if (kKind == 2) return (kB ? b : a)[c * M + m];
+  if (kKind == 3) {
+    if (!kB) return reinterpret_cast<const double* const*>(a)[m][as + c];
+    return restrict_at(reinterpret_cast<const double* const*>(b)[m], 2 * nxc, i, j);
+  }
+  if (!kB) return a[(long long)m * as + c];
+  return kKind == 1 ? restrict_at(b + (long long)m * bs, 2 * nxc, i, j) : b[(long long)m * bs + c];
+}
+
+// Stage ensemble kB of the CTA's cells into the columns col[cl * LD + m].
+template <int kKind, bool kB>
+__device__ __forceinline__ void w1_stage(int M, long long n, long long c0, int nxc, const double* a,
+                                         long long as, const double* b, long long bs, double* col,
+                                         int LD) {
   if (kKind == 2) {
-    va = a[c * M + m];
-    vb = b[c * M + m];
-  } else if (kKind == 3) {
-    va = reinterpret_cast<const double* const*>(a)[m][as + c];
-    vb = restrict_at(reinterpret_cast<const double* const*>(b)[m], 2 * nxc, i, j);
-  } else {
-    va = a[(long long)m * as + c];
-    vb = kKind == 1 ? restrict_at(b + (long long)m * bs, 2 * nxc, i, j) : b[(long long)m * bs + c];
+#pragma unroll 4
+    for (int e = threadIdx.x; e < M * kW1Cells; e += blockDim.x) {
+      const int cl = e / M, m = e - cl * M;
+      const long long c = c0 + cl;
+      col[cl * LD + m] = c < n ? w1_load<kKind, kB>(M, c, m, nxc, 0, 0, a, as, b, bs) : 0.0;
+    }
+    return;
+  }
+  // element e = m * kW1Cells + cl with e = threadIdx.x + k * blockDim.x: a
+  // thread keeps ONE cell (cl) for all its samples, so the cell's coarse
+  // coordinates (a 64-bit division) are found once; kStage samples' loads are
+  // issued before the first is stored (the staging is latency-bound)
+  constexpr int kStage = 8, kStep = 32;  // kStep = blockDim.x / kW1Cells samples apart
+  const int cl = threadIdx.x % kW1Cells;
+  const long long c = c0 + cl;
+  int i = 0, j = 0;
+  if (kB && kKind != 0 && c < n) {
+    const long long cg = (kKind == 3 ? as : 0) + c;
+    j = (int)(cg / nxc);
+    i = (int)(cg - (long long)j * nxc);
+  }
+  for (int m0 = threadIdx.x / kW1Cells; m0 < M; m0 += kStage * kStep) {
+    double v[kStage];
+#pragma unroll
+    for (int q = 0; q < kStage; ++q) {
+      const int m = m0 + q * kStep;
+      v[q] = (m < M && c < n) ? w1_load<kKind, kB>(M, c, m, nxc, i, j, a, as, b, bs) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < kStage; ++q) {
+      const int m = m0 + q * kStep;
+      if (m < M) col[cl * LD + m] = v[q];
+    }
   }
 }
 
@@ -592,58 +610,21 @@ __global__ void __launch_bounds__(32 * kW1Cells, 4) k_w1_tile(int M, long long n
                                                            const double* b, long long bs,
                                                            double* terms) {
   extern __shared__ double smw[];
-  constexpr int LD = 32 * R + 32;  // column stride: transposed stores, merge scratch e + e/32
-  double* sa = smw;
-  double* sb = smw + kW1Cells * LD;
+  constexpr int LD = 32 * R + 32;  // column stride (the merge sort's scratch: e + e/32)
   const long long c0 = (long long)blockIdx.x * kW1Cells;
-  if (kKind == 2) {
-#pragma unroll 4
-    for (int e = threadIdx.x; e < M * kW1Cells; e += blockDim.x) {
-      const int cl = e / M, m = e - cl * M;
-      const long long c = c0 + cl;
-      double va = 0.0, vb = 0.0;
-      if (c < n) w1_load<kKind>(M, c, m, nxc, 0, 0, a, as, b, bs, va, vb);
-      sa[cl * LD + m] = va;
-      sb[cl * LD + m] = vb;
-    }
-  } else {
-    // element e = m * kW1Cells + cl with e = threadIdx.x + k * blockDim.x: a
-    // thread keeps ONE cell (cl) for all its samples, so the cell's coarse
-    // coordinates (a 64-bit division) are found once; kStage samples' loads
-    // are issued before the first is stored (the staging is latency-bound)
-    constexpr int kStage = 8, kStep = 32;  // kStep = blockDim.x / kW1Cells samples apart
-    const int cl = threadIdx.x % kW1Cells;
-    const long long c = c0 + cl;
-    int i = 0, j = 0;
-    if (kKind != 0 && c < n) {
-      const long long cg = (kKind == 3 ? as : 0) + c;
-      j = (int)(cg / nxc);
-      i = (int)(cg - (long long)j * nxc);
-    }
-    for (int m0 = threadIdx.x / kW1Cells; m0 < M; m0 += kStage * kStep) {
-      double va[kStage], vb[kStage];
-#pragma unroll
-      for (int q = 0; q < kStage; ++q) {
-        const int m = m0 + q * kStep;
-        va[q] = vb[q] = 0.0;
-        if (m < M && c < n) w1_load<kKind>(M, c, m, nxc, i, j, a, as, b, bs, va[q], vb[q]);
-      }
-#pragma unroll
-      for (int q = 0; q < kStage; ++q) {
-        const int m = m0 + q * kStep;
-        if (m < M) {
-          sa[cl * LD + m] = va[q];
-          sb[cl * LD + m] = vb[q];
-        }
-      }
-    }
-  }
-  __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long c = c0 + w;
-  if (c >= n) return;
-  const double t = w1_cell<R>(M, lane, sa + w * LD, sb + w * LD);
-  if (lane == 0) terms[c] = t;
+  const bool live = c0 + w < n;
+  double sa[R], sb[R];
+  w1_stage<kKind, false>(M, n, c0, nxc, a, as, b, bs, smw, LD);
+  __syncthreads();
+  if (live) warp_sort_column<R>(M, lane, smw + w * LD, sa);
+  __syncthreads();  // every warp is done with its column
+  w1_stage<kKind, true>(M, n, c0, nxc, a, as, b, bs, smw, LD);
+  __syncthreads();
+  if (!live) return;
+  warp_sort_column<R>(M, lane, smw + w * LD, sb);
+  const double t = w1_rank_sum<R>(M, lane, sa, sb);
+  if (lane == 0) terms[c0 + w] = t;
 }
 
 // acc = sum_c terms[c] in storage order; result = acc / n (metrics.hpp:112-124).
@@ -796,8 +777,8 @@ __global__ void k_w1_keys(int M, long long c0, long long nb, int nxc, const doub
     const long long cl = cb + tx, c = c0 + cl;
     unsigned long long va = 0, vb = 0;
     if (m < M && cl < nb) {
-      double x, y;
-      w1_load<kKind>(M, c, m, nxc, ci, cj, a, as, b, bs, x, y);
+      const double x = w1_load<kKind, false>(M, c, m, nxc, ci, cj, a, as, b, bs);
+      const double y = w1_load<kKind, true>(M, c, m, nxc, ci, cj, a, as, b, bs);
       va = dkey(x);
       vb = dkey(y);
     }
@@ -895,7 +876,7 @@ static cudaError_t launch_w1(int M, long long n, int nxc, const double* a, long 
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kernel<<<grid, 32 * kW1Cells, smem, st>>>(M, n, nxc, a, as, b, bs, terms);
   };
-#define VLBM_W1_K(R) go(k_w1_tile<R, kKind>, R, 2)
+#define VLBM_W1_K(R) go(k_w1_tile<R, kKind>, R, 1)
   if (M <= 32)
     VLBM_W1_K(1);
   else if (M <= 64)
