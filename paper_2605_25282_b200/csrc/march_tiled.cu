@@ -544,6 +544,20 @@ __global__ void __launch_bounds__(256, 2) k_theta_hard(MarchParams P) {
         P.theta[idx] = rlmp_theta_hard_plain(fo, cf, b, gm1);  // never seen on a running sample
       } else {
         h = rlmp_hard_stage(fo, cf, delta, b, gm1);
+        if (P.audit && h.form >= 0) {
+          // audit of the stage's quadratic-form decisions at thc: the vertex
+          // floors and every margin bit against their exact evaluations
+          bool bad = (h.form > 0) != vertex_floors_ok(h.thc, fo, cf, b, gm1);
+          const cs t[4] = {scale(h.thc, cf[0]), scale(h.thc, cf[1]), scale(h.thc, cf[2]),
+                           scale(h.thc, cf[3])};
+          for (unsigned m = h.mhi; m; m &= m - 1u) {
+            const cs v = vertex_at(fo, t, __ffs(m) - 1);
+            const double p = pressure(v, gm1);
+            bad = bad || !vertex_margin(p, p, v.r, v.r, b, h.err, h.er);
+          }
+          if (bad) atomicAdd(P.audit, 1ull);
+          atomicAdd(P.audit + 13, 1ull);  // [13] stages decided by the form
+        }
         if (h.done) {
           P.theta[idx] = h.result;
         } else {

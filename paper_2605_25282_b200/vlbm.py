@@ -413,7 +413,8 @@ class BatchSimulation:
         return dict(mismatches=n[0], bisections=n[1], certified_at_thc=n[2], uncertified=n[3],
                     not_certifiable=n[4], no_margin_at_0=n[5], unc_vertices_start=n[6],
                     vertex_evals=n[7], diag_ok_at_1=n[8], vertex_decided_at_1=n[9],
-                    feasible_at_1=n[10], vertex_open_at_1=n[12])
+                    feasible_at_1=n[10], vertex_open_at_1=n[12],
+                    stage_decided_by_form=n[13])
 
     def audit_mismatches(self) -> int:
         return self.audit_counters()["mismatches"]

@@ -130,14 +130,68 @@ int main(int argc, char** argv) {
     ++hyp_n;
     hyp_bad += !same(want, got);
   }
+  // vertex_floors_quadform against the exact vertex checks on synthetic cells
+  // built to sit ON the pressure floor: a jet-core state (kinetic energy up to
+  // 1e8 x pressure), corrections of relative size 1e-1 .. 1e-12, the energy
+  // tuned so that one vertex pressure lands within ~1e-17 .. 1e-9 (relative to
+  // its kinetic energy) of the floor, either side (for every second cell it
+  // is the smallest of the 15); plus zero / negative
+  // densities and non-finite components.  Both decided answers must be right.
+  long fz_n = 0, fz_pass = 0, fz_fail = 0, fz_open = 0, fz_bad = 0;
+  {
+    auto uni = [&] { return (double)(next() >> 11) * 0x1p-53; };
+    for (int q = 0; q < 600000; ++q) {
+      const double rho = std::ldexp(0.5 + uni(), (int)(next() % 5) - 2);
+      const double vel = std::ldexp(1.0 + uni(), (int)(next() % 12));  // up to ~4000
+      const double ang = 6.283185307179586 * uni();
+      const double pr = std::ldexp(0.3 + uni(), (int)(next() % 6) - 3);
+      cs fo = {rho, rho * vel * std::cos(ang), rho * vel * std::sin(ang),
+               pr / gm1 + 0.5 * rho * vel * vel};
+      cs cf[4];
+      const double rel = std::ldexp(1.0, -(int)(next() % 40) - 3);
+      for (int f = 0; f < 4; ++f)
+        cf[f] = {fo.r * rel * (2 * uni() - 1), fo.mx * rel * (2 * uni() - 1) + rel * (uni() - 0.5),
+                 fo.my * rel * (2 * uni() - 1) + rel * (uni() - 0.5), fo.e * rel * (2 * uni() - 1)};
+      RlmpBounds b = {0, 0, 0, 0, 1e-12 * (0.5 + uni()), 1e-12 * (0.5 + uni())};
+      if (q % 7 == 0) b.p_floor = 0.0;
+      // move the energy so that vertex S's pressure is the floor + eps * K
+      const int S = 1 + (int)(next() % 15);
+      cs v = vertex_at(fo, cf, S);
+      const double K = 0.5 * (v.mx * v.mx + v.my * v.my) / v.r;
+      const double eps = std::ldexp(uni() - 0.5, -(int)(next() % 28) - 28);
+      fo.e += (b.p_floor / gm1 + K + eps * K) - v.e;
+      if (q & 1) {  // ... or the SMALLEST vertex pressure (exercises the all-pass decision)
+        double pmin = kInf, kmin = 0.0;
+        for (int m = 1; m < 16; ++m) {
+          const cs w = vertex_at(fo, cf, m);
+          const double pw = pressure(w, gm1);
+          if (pw < pmin) pmin = pw, kmin = 0.5 * (w.mx * w.mx + w.my * w.my) / w.r;
+        }
+        fo.e += ((b.p_floor + eps * kmin) - pmin) / gm1;
+      }
+      if (q % 1000 == 1) fo.r = -fo.r;
+      if (q % 1000 == 2) cf[q % 4].e = __longlong_as_double(0x7ff8000000000000ll);
+      if (q % 1000 == 3) cf[q % 4].mx = kInf;
+      if (q % 1000 == 4) fo.r = 0.0;
+      const bool ok = vertex_floors_ok(1.0, fo, cf, b, gm1);
+      const int d = vertex_floors_quadform(fo, cf, b.rho_floor, b.p_floor, gm1, 1.0 / gm1);
+      ++fz_n;
+      fz_pass += d == 1;
+      fz_fail += d == 0;
+      fz_open += d < 0;
+      fz_bad += (d == 1 && !ok) || (d == 0 && ok);
+    }
+  }
   std::printf(
       "{\"cells\": %ld, \"theta_one\": %ld, "
       "\"hard\": %ld, \"bisections\": %ld, \"replay_stopped\": %ld, \"mismatch_plain\": %ld, "
       "\"mismatch_queued\": %ld, \"mismatch_replay\": %ld, \"audit_errors\": %llu, "
       "\"margin_errors\": %ld, \"hypot_checks\": %ld, \"hypot_errors\": %ld, "
       "\"quadform_pass\": %ld, \"quadform_fail\": %ld, \"quadform_open\": %ld, "
-      "\"quadform_errors\": %ld}\n",
+      "\"quadform_errors\": %ld, \"fuzz_cells\": %ld, \"fuzz_pass\": %ld, \"fuzz_fail\": %ld, "
+      "\"fuzz_open\": %ld, \"fuzz_errors\": %ld}\n",
       cells, at_one, hard, bisect, stopped, bad_plain, bad_queued, bad_replay,
-      audit[0], margin_bad, hyp_n, hyp_bad, quad_pass, quad_fail, quad_open, quad_bad);
+      audit[0], margin_bad, hyp_n, hyp_bad, quad_pass, quad_fail, quad_open, quad_bad, fz_n, fz_pass,
+      fz_fail, fz_open, fz_bad);
   return 0;
 }

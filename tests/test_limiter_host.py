@@ -52,6 +52,9 @@ def test_limiter_paths_bit_exact(vo, limiter_check, tmp_path, m, steps, every):
     assert r["quadform_pass"] > 0.9 * r["theta_one"] and r["quadform_fail"] > 0
     assert r["quadform_open"] < 0.02 * r["cells"]
     assert r["hypot_checks"] > 100000  # hypot_ref (conservative bound) == this host's libm
-    for k in ("quadform_errors", "mismatch_plain", "mismatch_queued", "mismatch_replay",
+    # synthetic cells sitting on the pressure floor (both sides, jet-core cancellation,
+    # non-finite and non-positive densities): decided both ways, never wrongly
+    assert r["fuzz_pass"] > 50000 and r["fuzz_fail"] > 50000 and r["fuzz_open"] > 1000
+    for k in ("fuzz_errors", "quadform_errors", "mismatch_plain", "mismatch_queued", "mismatch_replay",
               "audit_errors", "margin_errors", "hypot_errors"):
         assert r[k] == 0, (k, r)
