@@ -528,13 +528,14 @@ __device__ __forceinline__ double w1_rank_sum(int M, int lane, const double (&sa
   return cell / static_cast<double>(M);
 }
 
-// A CTA of kW1Cells warps owns kW1Cells consecutive cells, one warp per cell,
-// with ONE shared-memory column [m] per cell (8.4 KB at M <= 1024: 16 warps
-// per SM where two columns allowed 12).  The M values of the first ensemble
-// for the CTA's cells are staged into the columns with sector-efficient loads
-// and each warp sorts its cell's column into registers; then the second
-// ensemble is staged into the SAME columns, sorted, and each warp adds its
-// cell's |a_(m) - b_(m)| in rank order.
+// A CTA of kW1Cells warps owns kW1Cells consecutive cells, one warp per cell.
+// The M values of both ensembles for the CTA's cells are staged into shared
+// memory columns [cell][m] with sector-efficient loads; each warp then sorts
+// its cell's first column into registers, parks it back in that column,
+// sorts the second column and adds |a_(m) - b_(m)| in rank order.  (One
+// column per cell, staged and sorted in turn, reaches 16 warps/SM instead of
+// 12 but measured slower, 27.5 vs 22.7 ms: two latency-bound staging phases
+// and three CTA barriers per tile.)
 //   kKind 0: sample-major planes, value(m, c) = a[m*as + c], b[m*bs + c]
 //   kKind 1: coarse planes vs the restriction of fine planes (b = fine,
 //            bs = fine sample stride; 32-byte coarse and two 64-byte fine
@@ -611,20 +612,86 @@ __global__ void __launch_bounds__(32 * kW1Cells, 4) k_w1_tile(int M, long long n
                                                            double* terms) {
   extern __shared__ double smw[];
   constexpr int LD = 32 * R + 32;  // column stride (the merge sort's scratch: e + e/32)
+  double* ca = smw;                  // [kW1Cells][LD] first ensemble
+  double* cb = smw + kW1Cells * LD;  // second ensemble
   const long long c0 = (long long)blockIdx.x * kW1Cells;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const bool live = c0 + w < n;
+  w1_stage<kKind, false>(M, n, c0, nxc, a, as, b, bs, ca, LD);
+  w1_stage<kKind, true>(M, n, c0, nxc, a, as, b, bs, cb, LD);
+  __syncthreads();
+  if (c0 + w >= n) return;
   double sa[R], sb[R];
-  w1_stage<kKind, false>(M, n, c0, nxc, a, as, b, bs, smw, LD);
-  __syncthreads();
-  if (live) warp_sort_column<R>(M, lane, smw + w * LD, sa);
-  __syncthreads();  // every warp is done with its column
-  w1_stage<kKind, true>(M, n, c0, nxc, a, as, b, bs, smw, LD);
-  __syncthreads();
-  if (!live) return;
-  warp_sort_column<R>(M, lane, smw + w * LD, sb);
+  ca += w * LD;
+#pragma unroll 1
+  for (int pass = 0; pass < 2; ++pass) {  // one copy of the sort's code for both columns
+    warp_sort_column<R>(M, lane, pass ? cb + w * LD : ca, sb);
+    if (pass == 0) {
+      // the sorted first column is parked in its own (now free) shared column
+      // at slot (r, lane), so the second sort has the registers to itself
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < R; ++r) ca[r * 32 + lane] = sb[r];
+      __syncwarp();
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) sa[r] = ca[r * 32 + lane];
   const double t = w1_rank_sum<R>(M, lane, sa, sb);
   if (lane == 0) terms[c0 + w] = t;
+}
+
+// Warp-autonomous variant (A/B: VLBM_W1_WARP=1): each warp stages its own
+// cell's column, one ensemble at a time into ONE column (16 warps/SM), with no
+// CTA barrier; the four warps of a CTA take adjacent cells, so the sectors a
+// warp uses only a quarter (coarse) or half (fine rows) of are hit in L1/L2 by
+// its neighbours.
+template <int R, int kKind>
+__global__ void __launch_bounds__(32 * kW1Cells, 4) k_w1_warp(int M, long long n, int nxc,
+                                                           const double* a, long long as,
+                                                           const double* b, long long bs,
+                                                           double* terms) {
+  extern __shared__ double smw[];
+  constexpr int LD = 32 * R + 32;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long c = (long long)blockIdx.x * kW1Cells + w;
+  if (c >= n) return;
+  double* col = smw + w * LD;
+  int i = 0, j = 0;
+  if (kKind == 1 || kKind == 3) {
+    const long long cg = (kKind == 3 ? as : 0) + c;
+    j = (int)(cg / nxc);
+    i = (int)(cg - (long long)j * nxc);
+  }
+  constexpr int kStage = 8;
+  double sa[R], sb[R];
+#pragma unroll 1
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int m0 = lane; m0 < M; m0 += kStage * 32) {
+      double v[kStage];
+#pragma unroll
+      for (int q = 0; q < kStage; ++q) {
+        const int m = m0 + q * 32;
+        v[q] = 0.0;
+        if (m < M)
+          v[q] = pass ? w1_load<kKind, true>(M, c, m, nxc, i, j, a, as, b, bs)
+                      : w1_load<kKind, false>(M, c, m, nxc, i, j, a, as, b, bs);
+      }
+#pragma unroll
+      for (int q = 0; q < kStage; ++q) {
+        const int m = m0 + q * 32;
+        if (m < M) col[m] = v[q];
+      }
+    }
+    __syncwarp();
+    warp_sort_column<R>(M, lane, col, sb);
+    __syncwarp();  // every lane has gathered: the column is free
+    if (pass == 0) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) sa[r] = sb[r];
+    }
+  }
+  const double t = w1_rank_sum<R>(M, lane, sa, sb);
+  if (lane == 0) terms[c] = t;
 }
 
 // acc = sum_c terms[c] in storage order; result = acc / n (metrics.hpp:112-124).
@@ -876,7 +943,12 @@ static cudaError_t launch_w1(int M, long long n, int nxc, const double* a, long 
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kernel<<<grid, 32 * kW1Cells, smem, st>>>(M, n, nxc, a, as, b, bs, terms);
   };
-#define VLBM_W1_K(R) go(k_w1_tile<R, kKind>, R, 1)
+  static const bool warp_variant = [] {
+    const char* e = getenv("VLBM_W1_WARP");
+    return e && atoi(e) != 0;
+  }();
+#define VLBM_W1_K(R) \
+  (warp_variant ? go(k_w1_warp<R, kKind>, R, 1) : go(k_w1_tile<R, kKind>, R, 2))
   if (M <= 32)
     VLBM_W1_K(1);
   else if (M <= 64)
