@@ -27,6 +27,12 @@
 
 #include "internal.h"
 
+#ifndef VLBM_W1_SORT
+// W1 per-cell sort: 2 = 32-bit quantised keys + index through the bitonic
+// network, exact order restored among equal quantised keys (default);
+// 1 = per-lane sort + merge-path levels on 64-bit keys; 0 = 64-bit bitonic network
+#define VLBM_W1_SORT 2
+#endif
 
 namespace vlbm_dev {
 
@@ -375,54 +381,74 @@ __device__ __forceinline__ void warp_sort_u32(unsigned (&v)[R], int lane) {
   }
 }
 
-// Exact rank order of a cell's column by QUANTISED keys.  On return (true)
-// c[r] & 1023 is the slot of the value of rank e = lane*R + r among the M
-// values col[0..M) (ranks >= M: c[r] = ~0).  The order-preserving 64-bit key
-// of each value is reduced to 22 bits relative to the cell's own key range
-// (q = (key - kmin) >> sh with sh from the span kmax - kmin, warp-uniform) and
-// packed with the value's slot as one 32-bit word c = q << 10 | slot, so the
-// bitonic network's compare-exchange is one integer min and one max (a 64-bit
-// one costs 6-7 instructions).  q is monotone in the key, so the network
-// leaves the slots in exact key order except possibly inside runs of EQUAL q,
-// which are contiguous: only if some adjacent pair of the warp shares its q
-// (rare: M <= 1024 values over 4 M buckets; never when the whole span is below
-// 2^22 ulps, where q is the exact offset) the runs are put in exact order by
-// odd-even transposition passes over the flagged pairs, comparing the values'
-// keys through the column, until no pass swaps.  After 6 passes (long runs:
-// values packed far below the cell's range) it gives up and returns false: the
-// caller sorts the column with the 64-bit merge sort instead.
+// Sorted column by QUANTISED keys: out[r] = the value of rank e = lane*R + r
+// among the M values col[0..M) (ranks >= M: unspecified).  The order-
+// preserving 64-bit key of each value is reduced to 22 bits relative to the
+// cell's own range (q = (key - base) >> sh; base and sh from the smallest and
+// largest high words of the keys, warp-uniform) and packed with the value's
+// slot as one 32-bit word c = q << 10 | slot, so the bitonic network's
+// compare-exchange is one integer min and one max (a 64-bit one costs 6-7
+// instructions).  q is monotone in the key, so the network leaves the values
+// in exact order except possibly inside runs of EQUAL q, which are contiguous:
+// the values are gathered by slot, and only if some adjacent pair of the warp
+// shares its q (rare: M <= 1024 values over 4 M buckets) the runs are put in
+// exact key order by odd-even transposition passes over the flagged pairs
+// until no pass swaps (after 6 passes: the 64-bit merge sort of the gathered
+// values, with col as its scratch).  The result is the exact sorted order of
+// the keys, as from the 64-bit sorts; col is clobbered.
 template <int R>
-__device__ __forceinline__ bool warp_sort_slots(int M, int lane, const double* col,
-                                                unsigned (&c)[R]) {
+__device__ __forceinline__ void warp_sort_quantised(int M, int lane, double* col,
+                                                    double (&out)[R]) {
   static_assert(R * 32 <= 1024, "slot index takes 10 bits");
   static_assert(R >= 2, "the exact-order passes pair elements inside a lane");
-  unsigned long long kmin = ~0ull, kmax = 0ull;
+  unsigned c[R];
+  unsigned hmin = 0xffffffffu, hmax = 0u;
 #pragma unroll
-  for (int r = 0; r < R; ++r) {  // the key range (the column is read twice)
+  for (int r = 0; r < R; ++r) {  // the range of the keys' high words (the column is read twice)
     const int m = r * 32 + lane;
     if (m < M) {
-      const unsigned long long k = dkey(col[m]);
-      kmin = min(kmin, k);
-      kmax = max(kmax, k);
+      const unsigned h = (unsigned)(dkey(col[m]) >> 32);
+      hmin = min(hmin, h);
+      hmax = max(hmax, h);
     }
   }
+  hmin = __reduce_min_sync(kFull, hmin);
+  hmax = __reduce_max_sync(kFull, hmax);
+  // base and span of the keys: from the high words, or -- when they all agree
+  // (a tight cluster) -- from the low words too, so that q is the exact key
+  // offset whenever the whole cell spans fewer than 2^22 ulps (no equal-q
+  // runs among distinct values then)
+  unsigned lbase = 0u;
+  unsigned long long span = (((unsigned long long)(hmax - hmin) + 1ull) << 32) - 1ull;
+  if (hmin == hmax) {  // warp-uniform
+    unsigned lmin = 0xffffffffu, lmax = 0u;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    kmin = min(kmin, __shfl_xor_sync(kFull, kmin, o));
-    kmax = max(kmax, __shfl_xor_sync(kFull, kmax, o));
+    for (int r = 0; r < R; ++r) {
+      const int m = r * 32 + lane;
+      if (m < M) {
+        const unsigned l = (unsigned)dkey(col[m]);
+        lmin = min(lmin, l);
+        lmax = max(lmax, l);
+      }
+    }
+    lbase = __reduce_min_sync(kFull, lmin);
+    span = __reduce_max_sync(kFull, lmax) - lbase;
   }
-  // key - kmin <= span < 2^(64 - clz(span))  ->  q < 2^22
-  const int sh = max(0, 42 - __clzll((long long)(kmax - kmin)));
+  const unsigned long long base = ((unsigned long long)hmin << 32) | lbase;
+  // key - base <= span < 2^(64 - clz(span))  ->  q < 2^22
+  const int sh = max(0, 42 - __clzll((long long)span));
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int m = r * 32 + lane;
-    const unsigned long long d = (m < M ? dkey(col[m]) : kmin) - kmin;
+    const unsigned long long d = (m < M ? dkey(col[m]) : base) - base;
     c[r] = m < M ? ((unsigned)(d >> sh) << 10) | (unsigned)m
                  : 0xffffffffu;  // pads last (slots < M <= 1023 when there are pads)
   }
   warp_sort_u32<R>(c, lane);
-  // adjacent ranks with equal q: bit r = pair (e0 + r, e0 + r + 1), both < M
   const int e0 = lane * R;
+#pragma unroll
+  for (int r = 0; r < R; ++r) out[r] = e0 + r < M ? col[c[r] & 1023u] : 0.0;
+  // adjacent ranks with equal q: bit r = pair (e0 + r, e0 + r + 1), both < M
   const unsigned cnext = __shfl_down_sync(kFull, c[0], 1);
   unsigned eq = 0u;
 #pragma unroll
@@ -431,96 +457,115 @@ __device__ __forceinline__ bool warp_sort_slots(int M, int lane, const double* c
     const bool in = e0 + r + 1 < M && (r + 1 < R || lane < 31);
     eq |= (in && ((c[r] ^ cn) < 1024u)) ? 1u << r : 0u;
   }
-  if (!__any_sync(kFull, eq != 0u)) return true;
-  auto gt = [&](unsigned x, unsigned y) { return dkey(col[x & 1023u]) > dkey(col[y & 1023u]); };
+  if (!__any_sync(kFull, eq != 0u)) return;
+  auto gt = [](double x, double y) { return dkey(x) > dkey(y); };
   bool again = true;
-#pragma unroll 1
   for (int pass = 0; again; ++pass) {
-    if (pass == 6) return false;
+    if (pass == 6) {  // long runs (values packed far below the cell's range): the 64-bit
+                      // merge sort of the gathered values; col is free (every lane gathered)
+      unsigned long long k[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) k[r] = e0 + r < M ? dkey(out[r]) : ~0ull;
+      __syncwarp();
+      warp_merge_sort<R>(k, lane, reinterpret_cast<unsigned long long*>(col));
+#pragma unroll
+      for (int r = 0; r < R; ++r) out[r] = dval(k[r]);
+      return;
+    }
     bool sw = false;
 #pragma unroll
     for (int par = 0; par < 2; ++par) {
 #pragma unroll
       for (int r = par; r + 1 < R; r += 2) {
-        if ((eq >> r & 1u) && gt(c[r], c[r + 1])) {
-          const unsigned t = c[r];
-          c[r] = c[r + 1];
-          c[r + 1] = t;
+        if ((eq >> r & 1u) && gt(out[r], out[r + 1])) {
+          const double t = out[r];
+          out[r] = out[r + 1];
+          out[r + 1] = t;
           sw = true;
         }
       }
       if (((R - 1) & 1) == par) {  // the pair across the lane boundary: (lane, R-1) with (lane+1, 0)
-        const unsigned nx = __shfl_down_sync(kFull, c[0], 1);
-        const unsigned pv = __shfl_up_sync(kFull, c[R - 1], 1);
+        const double nx = __shfl_down_sync(kFull, out[0], 1);
+        const double pv = __shfl_up_sync(kFull, out[R - 1], 1);
         const unsigned eqp = __shfl_up_sync(kFull, eq, 1);
-        const bool up = (eq >> (R - 1) & 1u) && gt(c[R - 1], nx);           // lower side
-        const bool dn = lane > 0 && (eqp >> (R - 1) & 1u) && gt(pv, c[0]);  // upper side
-        if (up) c[R - 1] = nx;
-        if (dn) c[0] = pv;
+        const bool up = (eq >> (R - 1) & 1u) && gt(out[R - 1], nx);               // lower side
+        const bool dn = lane > 0 && (eqp >> (R - 1) & 1u) && gt(pv, out[0]);      // upper side
+        if (up) out[R - 1] = nx;
+        if (dn) out[0] = pv;
         sw = sw || up || dn;
       }
     }
     again = __any_sync(kFull, sw);
   }
-  return true;
-}
-
-// out[r] = the value of rank lane*R + r of the column (ranks >= M: +0), exact
-// key order: warp_sort_slots + a gather by slot; the 64-bit sorts for long
-// runs of equal quantised keys (merge sort, col is its scratch and is
-// clobbered) and for R = 1 (the network).  All lanes of the warp call it.
-template <int R>
-__device__ __forceinline__ void warp_sort_column(int M, int lane, double* col, double (&out)[R]) {
-  bool done = false;
-  if constexpr (R >= 2) {
-    unsigned c[R];
-    done = warp_sort_slots<R>(M, lane, col, c);
-    if (done) {
-#pragma unroll
-      for (int r = 0; r < R; ++r) out[r] = lane * R + r < M ? col[c[r] & 1023u] : 0.0;
-    }
-  }
-  if (!done) {
-    unsigned long long k[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int m = r * 32 + lane;
-      k[r] = m < M ? dkey(col[m]) : ~0ull;
-    }
-    if constexpr (R >= 2) {
-      __syncwarp();  // the column is free once every lane holds its keys
-      warp_merge_sort<R>(k, lane, reinterpret_cast<unsigned long long*>(col));
-    } else {
-      warp_sort_asc<R>(k, lane);
-    }
-#pragma unroll
-    for (int r = 0; r < R; ++r) out[r] = lane * R + r < M ? dval(k[r]) : 0.0;
-  }
 }
 
 // Per-cell term: sum_m |a_(m) - b_(m)| over sorted ranks, sequential in m,
-// divided by M (metrics.hpp:118-122), from the lane's sorted values of both
-// ensembles (rank e = lane*R + r): the terms in parallel, then the chain
-// visits the lanes in order, each adding its R terms, so the sum is strictly
+// divided by M (metrics.hpp:118-122).  Loader functors return sample m's
+// value of the warp's cell.
+// ca / cb: the cell's M values of each ensemble in shared memory (ca is
+// overwritten).  One ensemble is sorted at a time (R keys per lane in
+// registers); the sorted first column is parked in ca at slot (r, lane) so the
+// second sort has the registers to itself.  Rank e = lane*R + r; the chain
+// visits lanes in order, each adding its R terms, so the sum is strictly
 // sequential in rank as in the reference.
 template <int R>
-__device__ __forceinline__ double w1_rank_sum(int M, int lane, const double (&sa)[R],
-                                              const double (&sb)[R]) {
-  const int valid = M - lane * R;  // ranks of this lane that exist
-  double t[R];
+__device__ __forceinline__ double w1_cell(int M, int lane, double* ca, double* cb) {
+  double sb_[R];
+  if constexpr (VLBM_W1_SORT == 2 && R >= 2) {
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {  // one copy of the network's code for both columns
+      warp_sort_quantised<R>(M, lane, pass ? cb : ca, sb_);
+      if (pass == 0) {
+        __syncwarp();  // every lane has gathered from ca
 #pragma unroll
-  for (int r = 0; r < R; ++r) t[r] = fabs(sa[r] - sb[r]);
+        for (int r = 0; r < R; ++r) ca[r * 32 + lane] = sb_[r];
+        __syncwarp();
+      }
+    }
+  } else {
+  unsigned long long k[R];
+#pragma unroll 1
+  for (int pass = 0; pass < 2; ++pass) {
+    const double* col = pass ? cb : ca;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int m = r * 32 + lane;  // load slot order is free: sorting is order-free
+      k[r] = m < M ? dkey(col[m]) : ~0ull;
+    }
+#if VLBM_W1_SORT == 1
+    __syncwarp();  // the column is free once every lane holds its keys
+    warp_merge_sort<R>(k, lane,
+                       reinterpret_cast<unsigned long long*>(const_cast<double*>(col)));
+#else
+    warp_sort_asc<R>(k, lane);
+#endif
+    if (pass == 0) {
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < R; ++r) ca[r * 32 + lane] = dval(k[r]);
+      __syncwarp();
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) sb_[r] = dval(k[r]);
+  }
+  // terms |a_(e) - b_(e)| of the lane's own ranks in registers, all lanes in
+  // parallel (padded ranks contribute nothing); then only the dependent adds
+  // run lane after lane
+  const int valid = M - lane * R;  // ranks of this lane that exist
+#pragma unroll
+  for (int r = 0; r < R; ++r) sb_[r] = fabs(ca[r * 32 + lane] - sb_[r]);
   double cell = 0.0;
 #pragma unroll 1
   for (int L = 0; L < 32; ++L) {
     if (lane == L) {
       if (valid >= R) {  // a full lane: R unguarded dependent adds
 #pragma unroll
-        for (int r = 0; r < R; ++r) cell += t[r];
+        for (int r = 0; r < R; ++r) cell += sb_[r];
       } else {
 #pragma unroll
         for (int r = 0; r < R; ++r)
-          if (r < valid) cell += t[r];
+          if (r < valid) cell += sb_[r];
       }
     }
     cell = __shfl_sync(kFull, cell, L);
@@ -529,13 +574,8 @@ __device__ __forceinline__ double w1_rank_sum(int M, int lane, const double (&sa
 }
 
 // A CTA of kW1Cells warps owns kW1Cells consecutive cells, one warp per cell.
-// The M values of both ensembles for the CTA's cells are staged into shared
-// memory columns [cell][m] with sector-efficient loads; each warp then sorts
-// its cell's first column into registers, parks it back in that column,
-// sorts the second column and adds |a_(m) - b_(m)| in rank order.  (One
-// column per cell, staged and sorted in turn, reaches 16 warps/SM instead of
-// 12 but measured slower, 27.5 vs 22.7 ms: two latency-bound staging phases
-// and three CTA barriers per tile.)
+// The M values of both ensembles for its cells are staged into shared memory
+// [cell][m] with sector-efficient loads, then each warp reduces its cell.
 //   kKind 0: sample-major planes, value(m, c) = a[m*as + c], b[m*bs + c]
 //   kKind 1: coarse planes vs the restriction of fine planes (b = fine,
 //            bs = fine sample stride; 32-byte coarse and two 64-byte fine
@@ -548,60 +588,21 @@ __device__ __forceinline__ double w1_rank_sum(int M, int lane, const double (&sa
 //            restriction is fused as in kind 1
 constexpr int kW1Cells = 4;
 
-// Sample m's value of (launch-local) cell c in ensemble kB ? b : a; (i, j): the
-// cell's coarse coordinates (kinds 1 and 3), found once per thread.
-template <int kKind, bool kB>
-__device__ __forceinline__ double w1_load(int M, long long c, int m, int nxc, int i, int j,
-                                          const double* a, long long as, const double* b,
-                                          long long bs) {
-  if (kKind == 2) return (kB ? b : a)[c * M + m];
-  if (kKind == 3) {
-    if (!kB) return reinterpret_cast<const double* const*>(a)[m][as + c];
-    return restrict_at(reinterpret_cast<const double* const*>(b)[m], 2 * nxc, i, j);
-  }
-  if (!kB) return a[(long long)m * as + c];
-  return kKind == 1 ? restrict_at(b + (long long)m * bs, 2 * nxc, i, j) : b[(long long)m * bs + c];
-}
-
-// Stage ensemble kB of the CTA's cells into the columns col[cl * LD + m].
-template <int kKind, bool kB>
-__device__ __forceinline__ void w1_stage(int M, long long n, long long c0, int nxc, const double* a,
-                                         long long as, const double* b, long long bs, double* col,
-                                         int LD) {
+// Sample m's value pair of (launch-local) cell c for the W1 kernels; (i, j):
+// the cell's coarse coordinates (kinds 1 and 3), found once per thread.
+template <int kKind>
+__device__ __forceinline__ void w1_load(int M, long long c, int m, int nxc, int i, int j,
+                                        const double* a, long long as, const double* b,
+                                        long long bs, double& va, double& vb) {
   if (kKind == 2) {
-#pragma unroll 4
-    for (int e = threadIdx.x; e < M * kW1Cells; e += blockDim.x) {
-      const int cl = e / M, m = e - cl * M;
-      const long long c = c0 + cl;
-      col[cl * LD + m] = c < n ? w1_load<kKind, kB>(M, c, m, nxc, 0, 0, a, as, b, bs) : 0.0;
-    }
-    return;
-  }
-  // element e = m * kW1Cells + cl with e = threadIdx.x + k * blockDim.x: a
-  // thread keeps ONE cell (cl) for all its samples, so the cell's coarse
-  // coordinates (a 64-bit division) are found once; kStage samples' loads are
-  // issued before the first is stored (the staging is latency-bound)
-  constexpr int kStage = 8, kStep = 32;  // kStep = blockDim.x / kW1Cells samples apart
-  const int cl = threadIdx.x % kW1Cells;
-  const long long c = c0 + cl;
-  int i = 0, j = 0;
-  if (kB && kKind != 0 && c < n) {
-    const long long cg = (kKind == 3 ? as : 0) + c;
-    j = (int)(cg / nxc);
-    i = (int)(cg - (long long)j * nxc);
-  }
-  for (int m0 = threadIdx.x / kW1Cells; m0 < M; m0 += kStage * kStep) {
-    double v[kStage];
-#pragma unroll
-    for (int q = 0; q < kStage; ++q) {
-      const int m = m0 + q * kStep;
-      v[q] = (m < M && c < n) ? w1_load<kKind, kB>(M, c, m, nxc, i, j, a, as, b, bs) : 0.0;
-    }
-#pragma unroll
-    for (int q = 0; q < kStage; ++q) {
-      const int m = m0 + q * kStep;
-      if (m < M) col[cl * LD + m] = v[q];
-    }
+    va = a[c * M + m];
+    vb = b[c * M + m];
+  } else if (kKind == 3) {
+    va = reinterpret_cast<const double* const*>(a)[m][as + c];
+    vb = restrict_at(reinterpret_cast<const double* const*>(b)[m], 2 * nxc, i, j);
+  } else {
+    va = a[(long long)m * as + c];
+    vb = kKind == 1 ? restrict_at(b + (long long)m * bs, 2 * nxc, i, j) : b[(long long)m * bs + c];
   }
 }
 
@@ -611,86 +612,57 @@ __global__ void __launch_bounds__(32 * kW1Cells, 4) k_w1_tile(int M, long long n
                                                            const double* b, long long bs,
                                                            double* terms) {
   extern __shared__ double smw[];
-  constexpr int LD = 32 * R + 32;  // column stride (the merge sort's scratch: e + e/32)
-  double* ca = smw;                  // [kW1Cells][LD] first ensemble
-  double* cb = smw + kW1Cells * LD;  // second ensemble
+  constexpr int LD = 32 * R + 32;  // column stride: transposed stores, merge scratch e + e/32
+  double* sa = smw;
+  double* sb = smw + kW1Cells * LD;
   const long long c0 = (long long)blockIdx.x * kW1Cells;
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  w1_stage<kKind, false>(M, n, c0, nxc, a, as, b, bs, ca, LD);
-  w1_stage<kKind, true>(M, n, c0, nxc, a, as, b, bs, cb, LD);
+  if (kKind == 2) {
+#pragma unroll 4
+    for (int e = threadIdx.x; e < M * kW1Cells; e += blockDim.x) {
+      const int cl = e / M, m = e - cl * M;
+      const long long c = c0 + cl;
+      double va = 0.0, vb = 0.0;
+      if (c < n) w1_load<kKind>(M, c, m, nxc, 0, 0, a, as, b, bs, va, vb);
+      sa[cl * LD + m] = va;
+      sb[cl * LD + m] = vb;
+    }
+  } else {
+    // element e = m * kW1Cells + cl with e = threadIdx.x + k * blockDim.x: a
+    // thread keeps ONE cell (cl) for all its samples, so the cell's coarse
+    // coordinates (a 64-bit division) are found once; kStage samples' loads
+    // are issued before the first is stored (the staging is latency-bound)
+    constexpr int kStage = 8, kStep = 32;  // kStep = blockDim.x / kW1Cells samples apart
+    const int cl = threadIdx.x % kW1Cells;
+    const long long c = c0 + cl;
+    int i = 0, j = 0;
+    if (kKind != 0 && c < n) {
+      const long long cg = (kKind == 3 ? as : 0) + c;
+      j = (int)(cg / nxc);
+      i = (int)(cg - (long long)j * nxc);
+    }
+    for (int m0 = threadIdx.x / kW1Cells; m0 < M; m0 += kStage * kStep) {
+      double va[kStage], vb[kStage];
+#pragma unroll
+      for (int q = 0; q < kStage; ++q) {
+        const int m = m0 + q * kStep;
+        va[q] = vb[q] = 0.0;
+        if (m < M && c < n) w1_load<kKind>(M, c, m, nxc, i, j, a, as, b, bs, va[q], vb[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < kStage; ++q) {
+        const int m = m0 + q * kStep;
+        if (m < M) {
+          sa[cl * LD + m] = va[q];
+          sb[cl * LD + m] = vb[q];
+        }
+      }
+    }
+  }
   __syncthreads();
-  if (c0 + w >= n) return;
-  double sa[R], sb[R];
-  ca += w * LD;
-#pragma unroll 1
-  for (int pass = 0; pass < 2; ++pass) {  // one copy of the sort's code for both columns
-    warp_sort_column<R>(M, lane, pass ? cb + w * LD : ca, sb);
-    if (pass == 0) {
-      // the sorted first column is parked in its own (now free) shared column
-      // at slot (r, lane), so the second sort has the registers to itself
-      __syncwarp();
-#pragma unroll
-      for (int r = 0; r < R; ++r) ca[r * 32 + lane] = sb[r];
-      __syncwarp();
-    }
-  }
-#pragma unroll
-  for (int r = 0; r < R; ++r) sa[r] = ca[r * 32 + lane];
-  const double t = w1_rank_sum<R>(M, lane, sa, sb);
-  if (lane == 0) terms[c0 + w] = t;
-}
-
-// Warp-autonomous variant (A/B: VLBM_W1_WARP=1): each warp stages its own
-// cell's column, one ensemble at a time into ONE column (16 warps/SM), with no
-// CTA barrier; the four warps of a CTA take adjacent cells, so the sectors a
-// warp uses only a quarter (coarse) or half (fine rows) of are hit in L1/L2 by
-// its neighbours.
-template <int R, int kKind>
-__global__ void __launch_bounds__(32 * kW1Cells, 4) k_w1_warp(int M, long long n, int nxc,
-                                                           const double* a, long long as,
-                                                           const double* b, long long bs,
-                                                           double* terms) {
-  extern __shared__ double smw[];
-  constexpr int LD = 32 * R + 32;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long c = (long long)blockIdx.x * kW1Cells + w;
+  const long long c = c0 + w;
   if (c >= n) return;
-  double* col = smw + w * LD;
-  int i = 0, j = 0;
-  if (kKind == 1 || kKind == 3) {
-    const long long cg = (kKind == 3 ? as : 0) + c;
-    j = (int)(cg / nxc);
-    i = (int)(cg - (long long)j * nxc);
-  }
-  constexpr int kStage = 8;
-  double sa[R], sb[R];
-#pragma unroll 1
-  for (int pass = 0; pass < 2; ++pass) {
-    for (int m0 = lane; m0 < M; m0 += kStage * 32) {
-      double v[kStage];
-#pragma unroll
-      for (int q = 0; q < kStage; ++q) {
-        const int m = m0 + q * 32;
-        v[q] = 0.0;
-        if (m < M)
-          v[q] = pass ? w1_load<kKind, true>(M, c, m, nxc, i, j, a, as, b, bs)
-                      : w1_load<kKind, false>(M, c, m, nxc, i, j, a, as, b, bs);
-      }
-#pragma unroll
-      for (int q = 0; q < kStage; ++q) {
-        const int m = m0 + q * 32;
-        if (m < M) col[m] = v[q];
-      }
-    }
-    __syncwarp();
-    warp_sort_column<R>(M, lane, col, sb);
-    __syncwarp();  // every lane has gathered: the column is free
-    if (pass == 0) {
-#pragma unroll
-      for (int r = 0; r < R; ++r) sa[r] = sb[r];
-    }
-  }
-  const double t = w1_rank_sum<R>(M, lane, sa, sb);
+  const double t = w1_cell<R>(M, lane, sa + w * LD, sb + w * LD);
   if (lane == 0) terms[c] = t;
 }
 
@@ -844,8 +816,8 @@ __global__ void k_w1_keys(int M, long long c0, long long nb, int nxc, const doub
     const long long cl = cb + tx, c = c0 + cl;
     unsigned long long va = 0, vb = 0;
     if (m < M && cl < nb) {
-      const double x = w1_load<kKind, false>(M, c, m, nxc, ci, cj, a, as, b, bs);
-      const double y = w1_load<kKind, true>(M, c, m, nxc, ci, cj, a, as, b, bs);
+      double x, y;
+      w1_load<kKind>(M, c, m, nxc, ci, cj, a, as, b, bs, x, y);
       va = dkey(x);
       vb = dkey(y);
     }
@@ -943,12 +915,7 @@ static cudaError_t launch_w1(int M, long long n, int nxc, const double* a, long 
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kernel<<<grid, 32 * kW1Cells, smem, st>>>(M, n, nxc, a, as, b, bs, terms);
   };
-  static const bool warp_variant = [] {
-    const char* e = getenv("VLBM_W1_WARP");
-    return e && atoi(e) != 0;
-  }();
-#define VLBM_W1_K(R) \
-  (warp_variant ? go(k_w1_warp<R, kKind>, R, 1) : go(k_w1_tile<R, kKind>, R, 2))
+#define VLBM_W1_K(R) go(k_w1_tile<R, kKind>, R, 2)
   if (M <= 32)
     VLBM_W1_K(1);
   else if (M <= 64)
