@@ -155,6 +155,7 @@ __global__ void k_sched(MarchParams P, double target, double fixed_dt) {
     }
     c->dt = dt;
     c->a = P.dx / dt;
+    c->inv2a = 0.5 / c->a;
     c->active = 1;
     c->budget -= 1;
     c->smax_bits = 0ull;

@@ -32,6 +32,7 @@ struct SampleCtl {
   double t;             // Simulation::time_
   double dt;            // dt of the scheduled step
   double a;             // a = dx / dt of the scheduled step
+  double inv2a;         // 0.5 / a, formed once by k_sched (the kernels' per-thread division)
   double smax_inlet;    // max signal speed over the inlet rows (constant)
   unsigned long long smax_bits;  // max interior signal speed (bits; >0 doubles order as u64)
   int bad_signal;       // some cell had a non-finite signal speed (rho<=0, p<=0, NaN)

@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(tiled::NTT, VLBM_THETA_MINB)
   using namespace tiled;
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) unsigned long long bar;
-  __shared__ int s_next;
+  __shared__ int s_next, s_ns, s_nx0, s_ny0;  // the CTA's next tile and its sample / origin
   double* R = sm;                    // u [4][NR2] by TMA, then inv2a f/g, p: [9][NR2]
   double* RF = R + kStagedTheta * NR2;  // rfo[NF], pfo[NF]
   double* SP = sm + kThetaSP;        // populations [16][NAT] by TMA
@@ -304,14 +304,19 @@ __global__ void __launch_bounds__(tiled::NTT, VLBM_THETA_MINB)
   if (threadIdx.x == 0) mbar_init(&bar);
   __syncthreads();
   if (threadIdx.x == 0) issue(t);
+  // sample and origin of tile t: divisions by every thread for the first tile
+  // only, then by thread 0 for the next tile (broadcast with s_next)
+  int s = t / per_sample, x0, y0;
+  {
+    const int r = t - s * per_sample;
+    x0 = (r % tiles_x) * TX, y0 = (r / tiles_x) * TYT;
+  }
   for (unsigned it = 0; t < total; ++it) {
-    const int s = t / per_sample, r = t - s * per_sample;
-    const int x0 = (r % tiles_x) * TX, y0 = (r / tiles_x) * TYT;
     const SampleCtl* c = P.ctl + s;
     const int parity = c->parity;
     const double* src = state_src(P, s, parity);
     const double* rows = P.inlet + (long long)s * P.ny * 4;
-    const double inv2a = 0.5 / c->a;
+    const double inv2a = c->inv2a;
     int tn_claim = 0;
     if (threadIdx.x == 0) tn_claim = claim_start(t);
     mbar_wait(&bar, it & 1u);
@@ -411,9 +416,17 @@ __global__ void __launch_bounds__(tiled::NTT, VLBM_THETA_MINB)
     }
     // The staged buffers are free: prefetch the next tile (claimed before the
     // barrier, so every thread reads s_next right after it).
-    if (threadIdx.x == 0) s_next = claim_finish(tn_claim);
+    if (threadIdx.x == 0) {
+      const int tn = claim_finish(tn_claim);
+      s_next = tn;
+      if (tn < total) {
+        const int sn = tn / per_sample, rn = tn - sn * per_sample;
+        s_ns = sn, s_nx0 = (rn % tiles_x) * TX, s_ny0 = (rn / tiles_x) * TYT;
+      }
+    }
     __syncthreads();
     const int t_next = s_next;
+    const int ns = s_ns, nx0 = s_nx0, ny0 = s_ny0;
     if (threadIdx.x == 0 && t_next < total) issue(t_next);
 
     // feasible(1): the diagonal first; then the 15 vertex floors decided by
@@ -453,6 +466,7 @@ __global__ void __launch_bounds__(tiled::NTT, VLBM_THETA_MINB)
     const long long cell = (long long)s * P.plane + (long long)j * P.pitch + i;
     enqueue_hard(P, hard, cell, foC, cf, b, gm1);
     t = t_next;
+    s = ns, x0 = nx0, y0 = ny0;
   }
 }
 
@@ -766,7 +780,7 @@ __global__ void __launch_bounds__(tiled::NT, VLBM_ADV_MINB)
   const double* src = state_src(P, s, parity);
   double* dst = state_dst(P, s, parity);
   const double* rows = P.inlet + (long long)s * P.ny * 4;
-  const double inv2a = 0.5 / c->a;
+  const double inv2a = c->inv2a;
   const double gm1 = P.gm1, w = P.w;
   if (threadIdx.x == 0) mbar_init(&bar);
   __syncthreads();
