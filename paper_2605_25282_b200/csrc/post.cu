@@ -606,31 +606,6 @@ __device__ __forceinline__ void w1_load(int M, long long c, int m, int nxc, int 
   }
 }
 
-// L2 prefetch of the element (cell c2, sample m) a later CTA will stage: the
-// staging is DRAM-latency-bound (ncu: a third of the warps' stall time on its
-// loads), so each CTA asks L2 for the sectors of the CTA kW1Ahead blocks
-// behind it in the launch order while it sorts (plain planes, kinds 0 and 1).
-#ifndef VLBM_W1_AHEAD
-#define VLBM_W1_AHEAD 148
-#endif
-constexpr int kW1Ahead = VLBM_W1_AHEAD;
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
-template <int kKind>
-__device__ __forceinline__ void w1_prefetch(long long c2, int m, int nxc, int i2, int j2,
-                                            const double* a, long long as, const double* b,
-                                            long long bs) {
-  prefetch_l2(a + (long long)m * as + c2);
-  if (kKind == 1) {
-    const double* r0 = b + (long long)m * bs + (long long)(2 * j2) * (2 * nxc) + 2 * i2;
-    prefetch_l2(r0);
-    prefetch_l2(r0 + 2 * nxc);
-  } else {
-    prefetch_l2(b + (long long)m * bs + c2);
-  }
-}
-
 template <int R, int kKind>
 __global__ void __launch_bounds__(32 * kW1Cells, 4) k_w1_tile(int M, long long n, int nxc,
                                                            const double* a, long long as,
@@ -665,14 +640,6 @@ __global__ void __launch_bounds__(32 * kW1Cells, 4) k_w1_tile(int M, long long n
       j = (int)(cg / nxc);
       i = (int)(cg - (long long)j * nxc);
     }
-    // the same thread's element of the CTA kW1Ahead blocks on (L2 prefetch)
-    const long long c2 = c + (long long)kW1Ahead * kW1Cells;
-    const bool ahead = (kKind == 0 || kKind == 1) && kW1Ahead > 0 && c2 < n;
-    int i2 = 0, j2 = 0;
-    if (ahead && kKind == 1) {
-      j2 = (int)(c2 / nxc);
-      i2 = (int)(c2 - (long long)j2 * nxc);
-    }
     for (int m0 = threadIdx.x / kW1Cells; m0 < M; m0 += kStage * kStep) {
       double va[kStage], vb[kStage];
 #pragma unroll
@@ -680,13 +647,6 @@ __global__ void __launch_bounds__(32 * kW1Cells, 4) k_w1_tile(int M, long long n
         const int m = m0 + q * kStep;
         va[q] = vb[q] = 0.0;
         if (m < M && c < n) w1_load<kKind>(M, c, m, nxc, i, j, a, as, b, bs, va[q], vb[q]);
-      }
-      if (ahead) {
-#pragma unroll
-        for (int q = 0; q < kStage; ++q) {
-          const int m = m0 + q * kStep;
-          if (m < M) w1_prefetch<kKind>(c2, m, nxc, i2, j2, a, as, b, bs);
-        }
       }
 #pragma unroll
       for (int q = 0; q < kStage; ++q) {
