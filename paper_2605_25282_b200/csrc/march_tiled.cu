@@ -70,9 +70,13 @@ constexpr unsigned kAdvanceTx = sizeof(double) * 4 * NA;
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
 }
-__device__ __forceinline__ void mbar_init(unsigned long long* bar) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)) : "memory");
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count = 1) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
@@ -177,6 +181,32 @@ __device__ __forceinline__ void flux_cell(const double* U, int NU, double* F, in
   if (with_p) F[8 * NFs + q] = p;
 }
 
+// The same for two staged cells at once: both cells' loads, then both cells'
+// arithmetic in one block (six independent divisions in flight), then the
+// stores -- the values are flux_cell's, operation by operation.
+__device__ __forceinline__ void flux_cell_pair(const double* U, int NU, double* F, int NFs, int qa,
+                                               int qb, double inv2a, double gm1) {
+  const cs ua = {U[qa], U[NU + qa], U[2 * NU + qa], U[3 * NU + qa]};
+  const cs ub = {U[qb], U[NU + qb], U[2 * NU + qb], U[3 * NU + qb]};
+  const double pa = pressure(ua, gm1), pb = pressure(ub, gm1);
+  const double a1 = ua.mx / ua.r, b1 = ub.mx / ub.r;
+  const double a2 = ua.my / ua.r, b2 = ub.my / ub.r;
+  const double fa[8] = {ua.mx * inv2a,          (ua.mx * a1 + pa) * inv2a,
+                        (ua.my * a1) * inv2a,   ((ua.e + pa) * a1) * inv2a,
+                        ua.my * inv2a,          (ua.mx * a2) * inv2a,
+                        (ua.my * a2 + pa) * inv2a, ((ua.e + pa) * a2) * inv2a};
+  const double fb[8] = {ub.mx * inv2a,          (ub.mx * b1 + pb) * inv2a,
+                        (ub.my * b1) * inv2a,   ((ub.e + pb) * b1) * inv2a,
+                        ub.my * inv2a,          (ub.mx * b2) * inv2a,
+                        (ub.my * b2 + pb) * inv2a, ((ub.e + pb) * b2) * inv2a};
+#pragma unroll
+  for (int k = 0; k < 8; ++k) F[k * NFs + qa] = fa[k];
+  F[8 * NFs + qa] = pa;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) F[k * NFs + qb] = fb[k];
+  F[8 * NFs + qb] = pb;
+}
+
 __device__ __forceinline__ cs plane4(const double* A, int N, int q) {
   return {A[q], A[N + q], A[2 * N + q], A[3 * N + q]};
 }
@@ -262,8 +292,14 @@ __global__ void __launch_bounds__(tiled::NTT, VLBM_THETA_MINB)
                   const __grid_constant__ CUtensorMap tmp1) {
   using namespace tiled;
   extern __shared__ __align__(128) double sm[];
-  __shared__ __align__(8) unsigned long long bar;
-  __shared__ int s_next, s_ns, s_nx0, s_ny0;  // the CTA's next tile and its sample / origin
+  // bar: the tile's TMA loads have landed; bar_free: every warp has taken its
+  // last value from the staged tile (one arrival per warp), so thread 0 may
+  // overwrite the buffers with the next tile's loads
+  __shared__ __align__(8) unsigned long long bar, bar_free;
+  // the CTA's current tile, written by thread 0 before it issues the tile's
+  // loads (ordered before every other thread's read by the mbarrier)
+  __shared__ int s_next, s_ns, s_nx0, s_ny0, s_par;
+  __shared__ double s_inv2a;
   double* R = sm;                    // u [4][NR2] by TMA, then inv2a f/g, p: [9][NR2]
   double* RF = R + kStagedTheta * NR2;  // rfo[NF], pfo[NF]
   double* SP = sm + kThetaSP;        // populations [16][NAT] by TMA
@@ -280,8 +316,8 @@ __global__ void __launch_bounds__(tiled::NTT, VLBM_THETA_MINB)
   // counter (hq_n[6], reset by k_sched) so CTAs stay balanced whatever the
   // per-tile cost (boundary tiles, hard cells); static striding without queues
   // The claim's atomic is issued at the top of the tile (claim_start) and its
-  // result used only before the prefetch barrier (claim_finish), so its
-  // round trip overlaps the tile's work.
+  // result used only when the tile's staged data has been consumed
+  // (claim_finish), so its round trip overlaps the tile's work.
   auto claim_start = [&](int t) {
     return P.hq_n ? (int)gridDim.x + atomicAdd(P.hq_n + 6, 1) : next_active(t + (int)gridDim.x);
   };
@@ -291,42 +327,63 @@ __global__ void __launch_bounds__(tiled::NTT, VLBM_THETA_MINB)
         tn = (int)gridDim.x + atomicAdd(P.hq_n + 6, 1);
     return tn;
   };
-  auto issue = [&](int t) {  // thread 0: the tile's TMA loads
+  // thread 0: publish tile t (sample, origin, buffer parity, 0.5/a) and issue
+  // its TMA loads; past the last tile a plain arrival completes the phase so
+  // that the waiting threads wake up and leave
+  auto publish = [&](int t) {
+    s_next = t;
+    if (t >= total) {
+      mbar_arrive(&bar);
+      return;
+    }
     const int s = t / per_sample, r = t - s * per_sample;
     const int x0 = (r % tiles_x) * TX, y0 = (r / tiles_x) * TYT;
     const int parity = P.ctl[s].parity;
+    s_ns = s, s_nx0 = x0, s_ny0 = y0, s_par = parity;
+    s_inv2a = P.ctl[s].inv2a;
     mbar_expect_tx(&bar, kThetaTx);
     tma_load_4d(R, parity ? &tmu1 : &tmu0, &bar, x0 - 2, y0 - 2, 0, s);
     if (!VLBM_THETA_GPOP) tma_load_4d(SP, parity ? &tmp1 : &tmp0, &bar, x0 - 2, y0 - 1, 4, s);
   };
-  int t = next_active(blockIdx.x);
-  if (t >= total) return;
-  if (threadIdx.x == 0) mbar_init(&bar);
-  __syncthreads();
-  if (threadIdx.x == 0) issue(t);
-  // sample and origin of tile t: divisions by every thread for the first tile
-  // only, then by thread 0 for the next tile (broadcast with s_next)
-  int s = t / per_sample, x0, y0;
   {
-    const int r = t - s * per_sample;
-    x0 = (r % tiles_x) * TX, y0 = (r / tiles_x) * TYT;
+    const int t0 = next_active(blockIdx.x);
+    if (t0 >= total) return;
+    if (threadIdx.x == 0) {
+      mbar_init(&bar);
+      mbar_init(&bar_free, NTT / 32);
+      publish(t0);
+    }
+    __syncthreads();
   }
-  for (unsigned it = 0; t < total; ++it) {
-    const SampleCtl* c = P.ctl + s;
-    const int parity = c->parity;
+  for (unsigned it = 0;; ++it) {
+    mbar_wait(&bar, it & 1u);
+    const int t = s_next;
+    if (t >= total) break;
+    const int s = s_ns, x0 = s_nx0, y0 = s_ny0, parity = s_par;
+    const double inv2a = s_inv2a;
     const double* src = state_src(P, s, parity);
     const double* rows = P.inlet + (long long)s * P.ny * 4;
-    const double inv2a = c->inv2a;
     int tn_claim = 0;
     if (threadIdx.x == 0) tn_claim = claim_start(t);
-    mbar_wait(&bar, it & 1u);
     if (!(x0 >= 2 && x0 + TX + 2 <= P.nx && y0 >= 2 && y0 + TYT + 2 <= P.ny)) {
       patch_box<false>(P, src, rows, R, RX2, RY2, x0 - 2, y0 - 2, inv2a);
       if (!VLBM_THETA_GPOP) patch_box<true>(P, src, rows, SP, AX, AYT, x0 - 2, y0 - 1, inv2a);
       __syncthreads();
     }
     double* F = R + 4 * NR2;
-    for (int q = threadIdx.x; q < NR2; q += NTT) flux_cell(R, NR2, F, NR2, q, inv2a, gm1, true);
+    {
+      // NR2 staged cells on NTT threads: the warps with a second cell take
+      // both in one straight-line block, so the two cells' division chains
+      // overlap (a warp whose second round is part-filled repeats the last
+      // cell: same values to the same addresses)
+      static_assert(NR2 > NTT && NR2 <= 2 * NTT, "one or two staged cells per thread");
+      const int q0 = threadIdx.x;
+      if ((q0 & ~31) + NTT < NR2) {
+        flux_cell_pair(R, NR2, F, NR2, q0, min(q0 + NTT, NR2 - 1), inv2a, gm1);
+      } else {
+        flux_cell(R, NR2, F, NR2, q0, inv2a, gm1, true);
+      }
+    }
     __syncthreads();
 
     // First-order candidates (compute_candidates, solver.hpp:301-316) on the
@@ -414,20 +471,17 @@ __global__ void __launch_bounds__(tiled::NTT, VLBM_THETA_MINB)
       b = rlmp_bounds(st, P.kappa, P.rho_floor_coef, P.p_floor_coef);
       delta = add(add(cf[0], cf[1]), add(cf[2], cf[3]));
     }
-    // The staged buffers are free: prefetch the next tile (claimed before the
-    // barrier, so every thread reads s_next right after it).
+    // This warp has taken its last value from the staged tile.  Thread 0 waits
+    // for every warp's arrival (no CTA barrier: the other warps go straight on
+    // to their feasibility work) and then issues the next tile's loads into
+    // the same buffers, so the loads overlap this tile's feasibility work.
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&bar_free);
     if (threadIdx.x == 0) {
       const int tn = claim_finish(tn_claim);
-      s_next = tn;
-      if (tn < total) {
-        const int sn = tn / per_sample, rn = tn - sn * per_sample;
-        s_ns = sn, s_nx0 = (rn % tiles_x) * TX, s_ny0 = (rn / tiles_x) * TYT;
-      }
+      mbar_wait(&bar_free, it & 1u);
+      publish(tn);
     }
-    __syncthreads();
-    const int t_next = s_next;
-    const int ns = s_ns, nx0 = s_nx0, ny0 = s_ny0;
-    if (threadIdx.x == 0 && t_next < total) issue(t_next);
 
     // feasible(1): the diagonal first; then the 15 vertex floors decided by
     // the quadratic form (rlmp.cuh::vertex_floors_quadform: no pressure
@@ -465,8 +519,6 @@ __global__ void __launch_bounds__(tiled::NTT, VLBM_THETA_MINB)
     }
     const long long cell = (long long)s * P.plane + (long long)j * P.pitch + i;
     enqueue_hard(P, hard, cell, foC, cf, b, gm1);
-    t = t_next;
-    s = ns, x0 = nx0, y0 = ny0;
   }
 }
 

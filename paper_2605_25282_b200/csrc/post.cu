@@ -330,6 +330,12 @@ __device__ __forceinline__ void warp_sort_u32(unsigned (&v)[R], int lane) {
     lo = min(a, b);
     hi = max(a, b);
   };
+  // the lane's side of a cross-lane compare-exchange: the upper lane keeps the
+  // larger key, the lower lane the smaller.  One compare (with the lane's side
+  // folded into its predicate) and one select, in place: written as
+  // upper ? max : min the runtime loops below carried a max, a predicated min
+  // and two register moves per key.
+  auto keep = [](unsigned a, unsigned o, bool upper) { return ((o < a) != upper) ? o : a; };
   // runs of R keys sorted inside each lane (merge sizes 2 .. R)
 #pragma unroll
   for (int k = 2; k <= R; k <<= 1) {
@@ -358,9 +364,9 @@ __device__ __forceinline__ void warp_sort_u32(unsigned (&v)[R], int lane) {
         const unsigned o1 = __shfl_xor_sync(kFull, v[q], m);
         if (q != r) {
           const unsigned o2 = __shfl_xor_sync(kFull, v[r], m);
-          v[q] = upper ? max(v[q], o2) : min(v[q], o2);
+          v[q] = keep(v[q], o2, upper);
         }
-        v[r] = upper ? max(v[r], o1) : min(v[r], o1);
+        v[r] = keep(v[r], o1, upper);
       }
     }
 #pragma unroll 1
@@ -369,7 +375,7 @@ __device__ __forceinline__ void warp_sort_u32(unsigned (&v)[R], int lane) {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const unsigned o = __shfl_xor_sync(kFull, v[r], h);
-        v[r] = upper ? max(v[r], o) : min(v[r], o);
+        v[r] = keep(v[r], o, upper);
       }
     }
 #pragma unroll
@@ -397,8 +403,8 @@ __device__ __forceinline__ void warp_sort_u32(unsigned (&v)[R], int lane) {
 // values, with col as its scratch).  The result is the exact sorted order of
 // the keys, as from the 64-bit sorts; col is clobbered.
 template <int R>
-__device__ __forceinline__ void warp_sort_quantised(int M, int lane, double* col,
-                                                    double (&out)[R]) {
+__device__ __forceinline__ void warp_sort_quantised(int M, int lane, unsigned long long* col,
+                                                    unsigned long long (&out)[R]) {
   static_assert(R * 32 <= 1024, "slot index takes 10 bits");
   static_assert(R >= 2, "the exact-order passes pair elements inside a lane");
   unsigned c[R];
@@ -407,7 +413,7 @@ __device__ __forceinline__ void warp_sort_quantised(int M, int lane, double* col
   for (int r = 0; r < R; ++r) {  // the range of the keys' high words (the column is read twice)
     const int m = r * 32 + lane;
     if (m < M) {
-      const unsigned h = (unsigned)(dkey(col[m]) >> 32);
+      const unsigned h = (unsigned)(col[m] >> 32);
       hmin = min(hmin, h);
       hmax = max(hmax, h);
     }
@@ -426,7 +432,7 @@ __device__ __forceinline__ void warp_sort_quantised(int M, int lane, double* col
     for (int r = 0; r < R; ++r) {
       const int m = r * 32 + lane;
       if (m < M) {
-        const unsigned l = (unsigned)dkey(col[m]);
+        const unsigned l = (unsigned)col[m];
         lmin = min(lmin, l);
         lmax = max(lmax, l);
       }
@@ -440,14 +446,14 @@ __device__ __forceinline__ void warp_sort_quantised(int M, int lane, double* col
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int m = r * 32 + lane;
-    const unsigned long long d = (m < M ? dkey(col[m]) : base) - base;
+    const unsigned long long d = (m < M ? col[m] : base) - base;
     c[r] = m < M ? ((unsigned)(d >> sh) << 10) | (unsigned)m
                  : 0xffffffffu;  // pads last (slots < M <= 1023 when there are pads)
   }
   warp_sort_u32<R>(c, lane);
   const int e0 = lane * R;
 #pragma unroll
-  for (int r = 0; r < R; ++r) out[r] = e0 + r < M ? col[c[r] & 1023u] : 0.0;
+  for (int r = 0; r < R; ++r) out[r] = e0 + r < M ? col[c[r] & 1023u] : ~0ull;  // pads last
   // adjacent ranks with equal q: bit r = pair (e0 + r, e0 + r + 1), both < M
   const unsigned cnext = __shfl_down_sync(kFull, c[0], 1);
   unsigned eq = 0u;
@@ -458,18 +464,12 @@ __device__ __forceinline__ void warp_sort_quantised(int M, int lane, double* col
     eq |= (in && ((c[r] ^ cn) < 1024u)) ? 1u << r : 0u;
   }
   if (!__any_sync(kFull, eq != 0u)) return;
-  auto gt = [](double x, double y) { return dkey(x) > dkey(y); };
   bool again = true;
   for (int pass = 0; again; ++pass) {
     if (pass == 6) {  // long runs (values packed far below the cell's range): the 64-bit
                       // merge sort of the gathered values; col is free (every lane gathered)
-      unsigned long long k[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r) k[r] = e0 + r < M ? dkey(out[r]) : ~0ull;
       __syncwarp();
-      warp_merge_sort<R>(k, lane, reinterpret_cast<unsigned long long*>(col));
-#pragma unroll
-      for (int r = 0; r < R; ++r) out[r] = dval(k[r]);
+      warp_merge_sort<R>(out, lane, col);
       return;
     }
     bool sw = false;
@@ -477,19 +477,19 @@ __device__ __forceinline__ void warp_sort_quantised(int M, int lane, double* col
     for (int par = 0; par < 2; ++par) {
 #pragma unroll
       for (int r = par; r + 1 < R; r += 2) {
-        if ((eq >> r & 1u) && gt(out[r], out[r + 1])) {
-          const double t = out[r];
+        if ((eq >> r & 1u) && out[r] > out[r + 1]) {
+          const unsigned long long t = out[r];
           out[r] = out[r + 1];
           out[r + 1] = t;
           sw = true;
         }
       }
       if (((R - 1) & 1) == par) {  // the pair across the lane boundary: (lane, R-1) with (lane+1, 0)
-        const double nx = __shfl_down_sync(kFull, out[0], 1);
-        const double pv = __shfl_up_sync(kFull, out[R - 1], 1);
+        const unsigned long long nx = __shfl_down_sync(kFull, out[0], 1);
+        const unsigned long long pv = __shfl_up_sync(kFull, out[R - 1], 1);
         const unsigned eqp = __shfl_up_sync(kFull, eq, 1);
-        const bool up = (eq >> (R - 1) & 1u) && gt(out[R - 1], nx);               // lower side
-        const bool dn = lane > 0 && (eqp >> (R - 1) & 1u) && gt(pv, out[0]);      // upper side
+        const bool up = (eq >> (R - 1) & 1u) && out[R - 1] > nx;               // lower side
+        const bool dn = lane > 0 && (eqp >> (R - 1) & 1u) && pv > out[0];      // upper side
         if (up) out[R - 1] = nx;
         if (dn) out[0] = pv;
         sw = sw || up || dn;
@@ -509,40 +509,46 @@ __device__ __forceinline__ void warp_sort_quantised(int M, int lane, double* col
 // visits lanes in order, each adding its R terms, so the sum is strictly
 // sequential in rank as in the reference.
 template <int R>
-__device__ __forceinline__ double w1_cell(int M, int lane, double* ca, double* cb) {
+__device__ __forceinline__ double w1_cell(int M, int lane, unsigned long long* ca,
+                                          unsigned long long* cb) {
+  // The columns hold the values' order-preserving KEYS (dkey, formed once by
+  // the staging threads): the sorts compare keys, and dval gives the values
+  // back for the terms.
   double sb_[R];
   if constexpr (VLBM_W1_SORT == 2 && R >= 2) {
+    unsigned long long kk[R];
 #pragma unroll 1
     for (int pass = 0; pass < 2; ++pass) {  // one copy of the network's code for both columns
-      warp_sort_quantised<R>(M, lane, pass ? cb : ca, sb_);
+      warp_sort_quantised<R>(M, lane, pass ? cb : ca, kk);
       if (pass == 0) {
         __syncwarp();  // every lane has gathered from ca
 #pragma unroll
-        for (int r = 0; r < R; ++r) ca[r * 32 + lane] = sb_[r];
+        for (int r = 0; r < R; ++r) ca[r * 32 + lane] = kk[r];
         __syncwarp();
       }
     }
+#pragma unroll
+    for (int r = 0; r < R; ++r) sb_[r] = dval(kk[r]);
   } else {
   unsigned long long k[R];
 #pragma unroll 1
   for (int pass = 0; pass < 2; ++pass) {
-    const double* col = pass ? cb : ca;
+    unsigned long long* col = pass ? cb : ca;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int m = r * 32 + lane;  // load slot order is free: sorting is order-free
-      k[r] = m < M ? dkey(col[m]) : ~0ull;
+      k[r] = m < M ? col[m] : ~0ull;
     }
 #if VLBM_W1_SORT == 1
     __syncwarp();  // the column is free once every lane holds its keys
-    warp_merge_sort<R>(k, lane,
-                       reinterpret_cast<unsigned long long*>(const_cast<double*>(col)));
+    warp_merge_sort<R>(k, lane, col);
 #else
     warp_sort_asc<R>(k, lane);
 #endif
     if (pass == 0) {
       __syncwarp();
 #pragma unroll
-      for (int r = 0; r < R; ++r) ca[r * 32 + lane] = dval(k[r]);
+      for (int r = 0; r < R; ++r) ca[r * 32 + lane] = k[r];
       __syncwarp();
     }
   }
@@ -554,7 +560,7 @@ __device__ __forceinline__ double w1_cell(int M, int lane, double* ca, double* c
   // run lane after lane
   const int valid = M - lane * R;  // ranks of this lane that exist
 #pragma unroll
-  for (int r = 0; r < R; ++r) sb_[r] = fabs(ca[r * 32 + lane] - sb_[r]);
+  for (int r = 0; r < R; ++r) sb_[r] = fabs(dval(ca[r * 32 + lane]) - sb_[r]);
   double cell = 0.0;
 #pragma unroll 1
   for (int L = 0; L < 32; ++L) {
@@ -611,10 +617,10 @@ __global__ void __launch_bounds__(32 * kW1Cells, 4) k_w1_tile(int M, long long n
                                                            const double* a, long long as,
                                                            const double* b, long long bs,
                                                            double* terms) {
-  extern __shared__ double smw[];
+  extern __shared__ unsigned long long smw[];  // the values' keys (dkey), [column][cell][m]
   constexpr int LD = 32 * R + 32;  // column stride: transposed stores, merge scratch e + e/32
-  double* sa = smw;
-  double* sb = smw + kW1Cells * LD;
+  unsigned long long* sa = smw;
+  unsigned long long* sb = smw + kW1Cells * LD;
   const long long c0 = (long long)blockIdx.x * kW1Cells;
   if (kKind == 2) {
 #pragma unroll 4
@@ -623,8 +629,8 @@ __global__ void __launch_bounds__(32 * kW1Cells, 4) k_w1_tile(int M, long long n
       const long long c = c0 + cl;
       double va = 0.0, vb = 0.0;
       if (c < n) w1_load<kKind>(M, c, m, nxc, 0, 0, a, as, b, bs, va, vb);
-      sa[cl * LD + m] = va;
-      sb[cl * LD + m] = vb;
+      sa[cl * LD + m] = dkey(va);
+      sb[cl * LD + m] = dkey(vb);
     }
   } else {
     // element e = m * kW1Cells + cl with e = threadIdx.x + k * blockDim.x: a
@@ -652,8 +658,8 @@ __global__ void __launch_bounds__(32 * kW1Cells, 4) k_w1_tile(int M, long long n
       for (int q = 0; q < kStage; ++q) {
         const int m = m0 + q * kStep;
         if (m < M) {
-          sa[cl * LD + m] = va[q];
-          sb[cl * LD + m] = vb[q];
+          sa[cl * LD + m] = dkey(va[q]);
+          sb[cl * LD + m] = dkey(vb[q]);
         }
       }
     }
