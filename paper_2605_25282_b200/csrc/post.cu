@@ -22,6 +22,7 @@
 #include <cub/device/device_segmented_sort.cuh>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdint>
 #include <cstdlib>
 
@@ -45,7 +46,6 @@ __device__ __forceinline__ double restrict_at(const double* f, int nxf, int i, i
   const double sum = ((r0[0] + r0[1]) + r1[0]) + r1[1];
   return sum * 0.25;
 }
-
 __global__ void k_restrict(int M, int nxc, int nyc, const double* fine, double* coarse) {
   const long long nc = (long long)nxc * nyc, nf = 4 * nc;
   const long long total = (long long)M * 4 * nc;
@@ -592,7 +592,16 @@ __device__ __forceinline__ double w1_cell(int M, int lane, unsigned long long* c
 //            fine plane, each on whichever GPU holds the sample (NVLink peer
 //            mapping); as = the first global cell of this launch; the
 //            restriction is fused as in kind 1
-constexpr int kW1Cells = 4;
+#ifndef VLBM_W1_CELLS
+#define VLBM_W1_CELLS 4
+#endif
+constexpr int kW1Cells = VLBM_W1_CELLS;
+#ifndef VLBM_W1_STAGE
+#define VLBM_W1_STAGE 8  // samples whose loads a staging thread keeps in flight
+#endif
+#ifndef VLBM_W1_MINB
+#define VLBM_W1_MINB 4  // register budget: 65536 / (128 threads x this)
+#endif
 
 // Sample m's value pair of (launch-local) cell c for the W1 kernels; (i, j):
 // the cell's coarse coordinates (kinds 1 and 3), found once per thread.
@@ -613,7 +622,7 @@ __device__ __forceinline__ void w1_load(int M, long long c, int m, int nxc, int 
 }
 
 template <int R, int kKind>
-__global__ void __launch_bounds__(32 * kW1Cells, 4) k_w1_tile(int M, long long n, int nxc,
+__global__ void __launch_bounds__(32 * kW1Cells, kW1Cells <= 4 ? VLBM_W1_MINB : 1) k_w1_tile(int M, long long n, int nxc,
                                                            const double* a, long long as,
                                                            const double* b, long long bs,
                                                            double* terms) {
@@ -632,43 +641,89 @@ __global__ void __launch_bounds__(32 * kW1Cells, 4) k_w1_tile(int M, long long n
       sa[cl * LD + m] = dkey(va);
       sb[cl * LD + m] = dkey(vb);
     }
+    __syncthreads();
   } else {
     // element e = m * kW1Cells + cl with e = threadIdx.x + k * blockDim.x: a
     // thread keeps ONE cell (cl) for all its samples, so the cell's coarse
     // coordinates (a 64-bit division) are found once; kStage samples' loads
-    // are issued before the first is stored (the staging is latency-bound)
-    constexpr int kStage = 8, kStep = 32;  // kStep = blockDim.x / kW1Cells samples apart
-    const int cl = threadIdx.x % kW1Cells;
+    // are issued before the first is stored (the staging is latency-bound).
+    // (Measured and dropped: the CTAs of a thread-block cluster staging 8 - 32
+    // consecutive cells together -- each CTA loading a share of the samples for
+    // all the cluster's cells in 64 - 512 B runs and writing the keys into the
+    // owners' columns through distributed shared memory: 20.7 / 24.0 / 26.0 ms
+    // with 2 / 4 / 8 CTAs per cluster against 20.4 ms.)
+    constexpr int kStage = VLBM_W1_STAGE, kStep = 32;  // kStep = blockDim.x / kW1Cells samples apart
+    const int cl = (int)threadIdx.x % kW1Cells;
     const long long c = c0 + cl;
     int i = 0, j = 0;
     if (kKind != 0 && c < n) {
-      const long long cg = (kKind == 3 ? as : 0) + c;
-      j = (int)(cg / nxc);
-      i = (int)(cg - (long long)j * nxc);
+      const long long cg_ = (kKind == 3 ? as : 0) + c;
+      j = (int)(cg_ / nxc);
+      i = (int)(cg_ - (long long)j * nxc);
     }
-    for (int m0 = threadIdx.x / kW1Cells; m0 < M; m0 += kStage * kStep) {
-      double va[kStage], vb[kStage];
+    unsigned long long* da = sa + cl * LD;
+    unsigned long long* db = sb + cl * LD;
+    // kVec: each fine row's pair as one 128-bit load (16-byte aligned pairs:
+    // an aligned plane and even strides -- every torch / cudaMalloc buffer),
+    // so neighbouring lanes read one contiguous run per row
+    auto stage = [&](auto vec_tag) {
+      constexpr bool kVec = decltype(vec_tag)::value;
+      for (int m0 = (int)threadIdx.x / kW1Cells; m0 < M; m0 += kStage * kStep) {
+        double va[kStage];
+        double2 f0[kStage], f1[kStage];  // the fine rows' pairs (kinds 1, 3); kind 0: b in f0.x
 #pragma unroll
-      for (int q = 0; q < kStage; ++q) {
-        const int m = m0 + q * kStep;
-        va[q] = vb[q] = 0.0;
-        if (m < M && c < n) w1_load<kKind>(M, c, m, nxc, i, j, a, as, b, bs, va[q], vb[q]);
-      }
+        for (int q = 0; q < kStage; ++q) {
+          const int m = m0 + q * kStep;
+          va[q] = 0.0;
+          f0[q] = f1[q] = make_double2(0.0, 0.0);
+          if (m < M && c < n) {
+            if (kKind == 0) {
+              va[q] = a[(long long)m * as + c];
+              f0[q].x = b[(long long)m * bs + c];
+            } else {
+              const double* fb = kKind == 3 ? reinterpret_cast<const double* const*>(b)[m]
+                                            : b + (long long)m * bs;
+              va[q] = kKind == 3 ? reinterpret_cast<const double* const*>(a)[m][as + c]
+                                 : a[(long long)m * as + c];
+              const double* r0 = fb + (long long)(2 * j) * (2 * nxc) + 2 * i;
+              const double* r1 = r0 + 2 * nxc;
+              if (kVec) {
+                f0[q] = *reinterpret_cast<const double2*>(r0);
+                f1[q] = *reinterpret_cast<const double2*>(r1);
+              } else {
+                f0[q] = make_double2(r0[0], r0[1]);
+                f1[q] = make_double2(r1[0], r1[1]);
+              }
+            }
+          }
+        }
 #pragma unroll
-      for (int q = 0; q < kStage; ++q) {
-        const int m = m0 + q * kStep;
-        if (m < M) {
-          sa[cl * LD + m] = dkey(va[q]);
-          sb[cl * LD + m] = dkey(vb[q]);
+        for (int q = 0; q < kStage; ++q) {
+          const int m = m0 + q * kStep;
+          if (m < M) {
+            // restrict_field's sum, operation by operation (restrict_at)
+            const double vb =
+                kKind == 0 ? f0[q].x : (((f0[q].x + f0[q].y) + f1[q].x) + f1[q].y) * 0.25;
+            da[m] = dkey(va[q]);
+            db[m] = dkey(vb);
+          }
         }
       }
-    }
+    };
+    if (kKind == 1 && (reinterpret_cast<unsigned long long>(b) & 15ull) == 0ull && (bs & 1) == 0)
+      stage(std::true_type{});
+    else
+      stage(std::false_type{});
+    __syncthreads();
   }
-  __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long c = c0 + w;
   if (c >= n) return;
+#ifdef VLBM_W1_EXP_NOSORT  // timing experiment only (WRONG results): the staging alone
+  const double t = dval(sa[w * LD + lane]) + dval(sb[w * LD + lane]);
+#else
   const double t = w1_cell<R>(M, lane, sa + w * LD, sb + w * LD);
+#endif
   if (lane == 0) terms[c] = t;
 }
 
