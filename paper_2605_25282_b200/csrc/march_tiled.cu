@@ -567,9 +567,10 @@ __device__ __forceinline__ int unc_class(unsigned unc) {
 // registers the next chunk's copies are issued into the same buffer, so
 // they overlap this chunk's work.
 __global__ void __launch_bounds__(256, 2) k_theta_hard(MarchParams P) {
-  __shared__ int nb, nc[3], baseb, basec[3];
   extern __shared__ __align__(128) double H[];  // [kHardWords][kHB] | idx[kHB]
-  __shared__ __align__(8) unsigned long long bar;
+  // bar: the chunk's bulk copies have landed; bar_free: every warp holds its
+  // entries in registers (one arrival per warp), the buffer may be refilled
+  __shared__ __align__(8) unsigned long long bar, bar_free;
   long long* HI = reinterpret_cast<long long*>(H + kHardWords * kHB);
   const int n = min(P.hq_n[0], P.hq_cap);
   const long long cap = P.hq_cap;
@@ -585,9 +586,11 @@ __global__ void __launch_bounds__(256, 2) k_theta_hard(MarchParams P) {
   };
   if (threadIdx.x == 0) {
     mbar_init(&bar);
+    mbar_init(&bar_free, 256 / 32);
     issue(blockIdx.x);
   }
   __syncthreads();
+  const unsigned lane = threadIdx.x & 31;
   for (int chunk = blockIdx.x, it = 0; chunk < nchunks; chunk += gridDim.x, ++it) {
     const int slot = chunk * kHB + threadIdx.x;
     int cls = 0;  // 0: finished here, 1: -> bq, 2: -> cq
@@ -601,8 +604,15 @@ __global__ void __launch_bounds__(256, 2) k_theta_hard(MarchParams P) {
       idx = HI[threadIdx.x];
       load_hard_staged(P, H, threadIdx.x, fo, cf, b);
     }
-    __syncthreads();  // the buffer is free: next chunk
-    if (threadIdx.x == 0 && chunk + (int)gridDim.x < nchunks) issue(chunk + gridDim.x);
+    // the buffer is free once every warp has arrived: thread 0 alone waits for
+    // that and issues the next chunk's copies; no CTA barrier in this loop, so
+    // no warp waits for another warp's slower branch of the stage
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&bar_free);
+    if (threadIdx.x == 0 && chunk + (int)gridDim.x < nchunks) {
+      mbar_wait(&bar_free, it & 1);
+      issue(chunk + gridDim.x);
+    }
     if (idx >= 0) {
       delta = add(add(cf[0], cf[1]), add(cf[2], cf[3]));
       if (!(finite4(fo) && finite4(cf[0]) && finite4(cf[1]) && finite4(cf[2]) && finite4(cf[3]) &&
@@ -636,19 +646,24 @@ __global__ void __launch_bounds__(256, 2) k_theta_hard(MarchParams P) {
         }
       }
     }
-    if (threadIdx.x == 0) nb = nc[0] = nc[1] = nc[2] = 0;
-    __syncthreads();
-    int my = 0;
-    if (cls == 1) my = atomicAdd(&nb, 1);
-    if (cls == 2) my = atomicAdd(&nc[ccls], 1);
-    __syncthreads();
-    // the four queue reservations by four warps' first lanes, in parallel
-    if (threadIdx.x == 0) baseb = nb ? atomicAdd(P.hq_n + 2, nb) : 0;
-    if (threadIdx.x >= 32 && threadIdx.x < 128 && (threadIdx.x & 31) == 0) {
-      const int k = (threadIdx.x >> 5) - 1;
-      basec[k] = nc[k] ? atomicAdd(P.hq_n + 3 + k, nc[k]) : 0;
+    // Queue slots, warp-aggregated: queue 0 = bq, 1..3 = the cq bins; lane k
+    // reserves queue k's slots for the warp (the four atomics are in flight
+    // together), every lane takes its rank among the warp's entries of its queue.
+    const int myq = cls == 1 ? 0 : (cls == 2 ? 1 + ccls : -1);
+    unsigned qm[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) qm[k] = __ballot_sync(0xffffffffu, myq == k);
+    int qbase = 0;
+    if (lane < 4) {
+      const unsigned m = lane == 0 ? qm[0] : (lane == 1 ? qm[1] : (lane == 2 ? qm[2] : qm[3]));
+      if (m) qbase = atomicAdd(P.hq_n + 2 + lane, __popc(m));
     }
-    __syncthreads();
+    int my = 0, nb = 0, baseb = 0;  // this lane's queue: rank, the warp's count and base
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int bk = __shfl_sync(0xffffffffu, qbase, k);
+      if (myq == k) my = __popc(qm[k] & ((1u << lane) - 1u)), nb = __popc(qm[k]), baseb = bk;
+    }
     const int third = P.hq_cap / 3;
     if (cls == 1) {
       const int s = baseb + my;
@@ -665,8 +680,8 @@ __global__ void __launch_bounds__(256, 2) k_theta_hard(MarchParams P) {
         P.theta[idx] = bisect_certified(fo, delta, b, h.thc, gm1);
       }
     } else if (cls == 2) {
-      const int s = ccls * third + basec[ccls] + my;
-      if (basec[ccls] + nc[ccls] <= third) {
+      const int s = ccls * third + baseb + my;
+      if (baseb + nb <= third) {
         double* q = P.cq + s;
         q[0] = fo.r, q[cap] = fo.mx, q[2 * cap] = fo.my, q[3 * cap] = fo.e;
 #pragma unroll
@@ -682,7 +697,7 @@ __global__ void __launch_bounds__(256, 2) k_theta_hard(MarchParams P) {
         q[27 * cap] = h.er;
         P.cq_idx[s] = idx | ((long long)h.mhi << 40) | ((long long)h.lo_all << 56);
       } else {
-        if (basec[ccls] + my < third) P.cq_idx[s] = -1;
+        if (baseb + my < third) P.cq_idx[s] = -1;
         if (P.qstats) atomicAdd(P.qstats, 1ull);
         P.theta[idx] = bisect_uncertified(fo, cf, delta, b, h, gm1, P.audit);
       }
