@@ -532,8 +532,8 @@ __global__ void __launch_bounds__(tiled::NTT, VLBM_THETA_MINB)
 //   k_bisect_unc    30 steps re-checking the uncertified vertices (replay on:
 //                   the bisection replayed, rlmp_replay.cuh)
 //   k_bisect_tail   the replayed bisections that need more exact steps
-// Queues use block-aggregated slots (one global atomic per CTA pass); a CTA
-// that would overflow a queue finishes those cells in place.
+// Queues use warp-aggregated slots (one global atomic per warp and queue); a
+// warp that would overflow a queue finishes those cells in place.
 // Hard-queue entries staged in shared memory: kHB consecutive slots, one
 // bulk copy per SoA word plane (kHardWords + the cell index).
 constexpr int kHB = 256;
