@@ -536,7 +536,11 @@ __global__ void __launch_bounds__(tiled::NTT, VLBM_THETA_MINB)
 // warp that would overflow a queue finishes those cells in place.
 // Hard-queue entries staged in shared memory: kHB consecutive slots, one
 // bulk copy per SoA word plane (kHardWords + the cell index).
-constexpr int kHB = 256;
+#ifndef VLBM_HARD_THREADS
+#define VLBM_HARD_THREADS 256  // k_theta_hard: threads per CTA = slots per staged chunk
+#define VLBM_HARD_MINB 2       // resident CTAs per SM (register budget)
+#endif
+constexpr int kHB = VLBM_HARD_THREADS;
 constexpr size_t kHardSmem = sizeof(double) * kHardWords * kHB + sizeof(long long) * kHB;
 __device__ __forceinline__ void load_hard_staged(const MarchParams& P, const double* H, int t,
                                                  cs& fo, cs* cf, RlmpBounds& b) {
@@ -566,7 +570,7 @@ __device__ __forceinline__ int unc_class(unsigned unc) {
 // shared memory by bulk copies; once every thread holds its entry in
 // registers the next chunk's copies are issued into the same buffer, so
 // they overlap this chunk's work.
-__global__ void __launch_bounds__(256, 2) k_theta_hard(MarchParams P) {
+__global__ void __launch_bounds__(kHB, VLBM_HARD_MINB) k_theta_hard(MarchParams P) {
   extern __shared__ __align__(128) double H[];  // [kHardWords][kHB] | idx[kHB]
   // bar: the chunk's bulk copies have landed; bar_free: every warp holds its
   // entries in registers (one arrival per warp), the buffer may be refilled
@@ -586,7 +590,7 @@ __global__ void __launch_bounds__(256, 2) k_theta_hard(MarchParams P) {
   };
   if (threadIdx.x == 0) {
     mbar_init(&bar);
-    mbar_init(&bar_free, 256 / 32);
+    mbar_init(&bar_free, kHB / 32);
     issue(blockIdx.x);
   }
   __syncthreads();
@@ -1047,7 +1051,7 @@ int theta_ctas_per_sm() {
 cudaError_t launch_theta_hard(const MarchParams& P, cudaStream_t st) {
   if (cudaError_t e = smem_attrs()) return e;
   if (P.hq) {
-    k_theta_hard<<<148 * 2, 256, kHardSmem, st>>>(P);
+    k_theta_hard<<<148 * VLBM_HARD_MINB, kHB, kHardSmem, st>>>(P);
     // the certified (diagonal-only) bisections run beside the uncertified
     // ones: disjoint cells and queues; joined before the advance
     cudaStream_t cs_ = st;

@@ -1029,7 +1029,13 @@ cudaError_t launch_w1_restrict_mean(int M, int nxc, int nyc, const double* a, in
                                     const double* f, int64_t fs, double* terms, double* acc,
                                     double* result, cudaStream_t st) {
   const long long n = (long long)nxc * nyc;
-  const int K = nyc >= 16 ? 16 : nyc;  // chunks of whole rows
+  // chunks of whole rows: 16 by default (VLBM_W1_CHUNKS: 1..16, measurement hook)
+  static const int k_env = [] {
+    const char* e = getenv("VLBM_W1_CHUNKS");
+    const int v = e ? atoi(e) : 16;
+    return v >= 1 && v <= 16 ? v : 16;
+  }();
+  const int K = nyc >= k_env ? k_env : nyc;
   // the second stream and its events: one set per host thread and device
   // (concurrent callers on several GPUs each get their own)
   struct Aux {
