@@ -537,8 +537,12 @@ __global__ void __launch_bounds__(tiled::NTT, VLBM_THETA_MINB)
 // Hard-queue entries staged in shared memory: kHB consecutive slots, one
 // bulk copy per SoA word plane (kHardWords + the cell index).
 #ifndef VLBM_HARD_THREADS
-#define VLBM_HARD_THREADS 256  // k_theta_hard: threads per CTA = slots per staged chunk
-#define VLBM_HARD_MINB 2       // resident CTAs per SM (register budget)
+// k_theta_hard: threads per CTA = slots per staged chunk, and resident CTAs
+// per SM (register budget).  128 x 3 (168 registers, no spills to speak of,
+// 12 warps/SM) measured 0.905 ms for the hard path against 0.930 for 256 x 2
+// (128 registers, 220 B of spills, 16 warps/SM); 128 x 4: 0.943, 512 x 1: 0.935
+#define VLBM_HARD_THREADS 128
+#define VLBM_HARD_MINB 3
 #endif
 constexpr int kHB = VLBM_HARD_THREADS;
 constexpr size_t kHardSmem = sizeof(double) * kHardWords * kHB + sizeof(long long) * kHB;
