@@ -770,7 +770,10 @@ constexpr int kReplayInline = VLBM_REPLAY_INLINE;
 #ifndef VLBM_UNC_MINB
 #define VLBM_UNC_MINB 2
 #endif
-__global__ void __launch_bounds__(256, VLBM_UNC_MINB) k_bisect_unc(MarchParams P) {
+#ifndef VLBM_UNC_THREADS
+#define VLBM_UNC_THREADS 256  // threads per CTA (the grid keeps its thread count)
+#endif
+__global__ void __launch_bounds__(VLBM_UNC_THREADS, VLBM_UNC_MINB) k_bisect_unc(MarchParams P) {
   const int third = P.hq_cap / 3;
   const int n = min(P.hq_n[3 + blockIdx.y], third);
   const long long cap = P.hq_cap;
@@ -818,7 +821,10 @@ __global__ void __launch_bounds__(256, VLBM_UNC_MINB) k_bisect_unc(MarchParams P
 }
 
 // The bisections k_bisect_unc stopped, finished with exact evaluations.
-__global__ void __launch_bounds__(128, 4) k_bisect_tail(MarchParams P) {
+#ifndef VLBM_TAIL_MINB
+#define VLBM_TAIL_MINB 4
+#endif
+__global__ void __launch_bounds__(128, VLBM_TAIL_MINB) k_bisect_tail(MarchParams P) {
   const int n = min(P.hq_n[7], P.hq_cap);
   const long long cap = P.hq_cap;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
@@ -1065,7 +1071,7 @@ cudaError_t launch_theta_hard(const MarchParams& P, cudaStream_t st) {
       cs_ = P.side;
     }
     k_bisect_cert<<<148 * VLBM_CERT_GRID, 256, 0, cs_>>>(P);
-    k_bisect_unc<<<dim3(148 * VLBM_UNC_GRID, 3), 256, 0, st>>>(P);
+    k_bisect_unc<<<dim3(148 * VLBM_UNC_GRID * (256 / VLBM_UNC_THREADS), 3), VLBM_UNC_THREADS, 0, st>>>(P);
     if (P.replay) k_bisect_tail<<<148 * VLBM_TAIL_GRID, 128, 0, st>>>(P);
     cudaError_t err = cudaGetLastError();
     if (P.side) {
