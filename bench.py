@@ -71,8 +71,18 @@ class ClockSampler:
 
     def __init__(self, device: int):
         self.device = device
-        self.rows = []
+        self.rows = []  # (arrival time, fields)
         self.proc = None
+        self.t0 = self.t1 = None
+
+    def begin(self):
+        """The timed region starts (the sampler itself is started earlier, under
+        the untimed run_to / warm-up load, so that nvidia-smi is already
+        streaming: a 20-step region lasts 60 ms, less than its start-up)."""
+        self.t0 = time.monotonic()
+
+    def end(self):
+        self.t1 = time.monotonic()
 
     def __enter__(self):
         try:
@@ -90,7 +100,7 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) == 6:
-                self.rows.append(parts)
+                self.rows.append((time.monotonic(), parts))
 
     def __exit__(self, *exc):
         if self.proc:
@@ -101,15 +111,20 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        if not self.rows:
+        # the samples of the timed region; the sampling period is 100 ms, so a
+        # short region also takes the samples within 150 ms of it (the GPU
+        # runs the same kernels, warm-up steps, right before it)
+        rows = [r for t, r in self.rows
+                if self.t0 is None or (self.t0 - 0.15 <= t <= (self.t1 or t) + 0.15)]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        reasons = sorted({n for r in self.rows for n, v in zip(self.NAMES, r[2:])
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        reasons = sorted({n for r in rows for n, v in zip(self.NAMES, r[2:])
                           if v.lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+                "samples": len(rows)}
 
 
 def fp64_profile():
@@ -510,20 +525,23 @@ def main():
     sim = v.BatchSimulation.jet(g, lat, gas, pp, base_seed=42, m0=rank * M, n_samples=M,
                                 device=local)
     stream = torch.cuda.ExternalStream(sim.stream(), device=torch.device("cuda", local))
-    if args.t_start > 0:
-        sim.run_to(args.t_start)
-    sim.step(args.warmup)
-    sim.set_timing(True)
-    st0 = sim.stats()
-    barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(local) as clk:  # started under the untimed load, see begin()
+        if args.t_start > 0:
+            sim.run_to(args.t_start)
+        sim.step(args.warmup)
+        sim.set_timing(True)
+        st0 = sim.stats()
+        barrier()
+        torch.cuda.synchronize()
+        clk.begin()
         ev0.record(stream)
         torch.cuda.nvtx.range_push("timed")  # ncu --nvtx-include timed/ (tools/kprof.sh)
         sim.step(args.steps)
         torch.cuda.nvtx.range_pop()
         ev1.record(stream)
         torch.cuda.synchronize()
+        clk.end()
     barrier()
     ms = ev0.elapsed_time(ev1)
     st1 = sim.stats()
